@@ -1,0 +1,444 @@
+#!/usr/bin/env python
+"""Benchmark of the separable PatchLift-NLM hot path (row pass -> column pass).
+
+Default workload (BASELINE.json configs[3], the config the metric is quoted on
+at 1/2/4/8 B200): c4 = 64 independent 2048x2048 integer-valued images, K=3,
+S=10, h=sqrt(14)*20, RC order.  With N GPUs the 64 images are split into
+contiguous shards, one per rank, with no communication (strong scaling: the
+batch is fixed).  ``--config c3|c2|c1|c5`` selects the other single-GPU
+workloads (c5 here runs its single-GPU form).
+
+One "step" = one RC over the whole (per-rank) batch, inputs resident in HBM.
+``value`` = all ranks' pixels / max-over-ranks device time (CUDA events).
+``e2e`` = the same metric through the C-ABI host entry point
+(pl_snlm_2d_row_col_host) with pinned host buffers, H2D + D2H inside.
+``--impl reference`` times the reference's own CPU implementation
+(oracle/_ref: the unmodified reference library, all host threads) on a bounded
+sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "separable PatchLift-NLM Mpixel/s at 1/2/4/8 B200; % of exp/FP32/HBM roofline"
+UNIT = "Mpixel/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c4", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------------------- dist
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def workload(cfg_name: str):
+    from paper_1407_2343_b200 import workloads as W
+    c = W.CONFIGS[cfg_name]
+    S, K, h = W.params(cfg_name)
+    return c, S, K, h
+
+
+def shard(n_items: int, world: int, rank: int):
+    lo = n_items * rank // world
+    hi = n_items * (rank + 1) // world
+    return lo, hi
+
+
+def make_inputs(cfg_name, lo, hi):
+    from paper_1407_2343_b200 import workloads as W
+    c = W.CONFIGS[cfg_name]
+    if c["kind"] == "signal":
+        return W.make_signal(c["n"], c["sigma"], seed=1)[None, :]
+    out = np.empty((hi - lo, c["rows"], c["cols"]), np.float32)
+    for k, b in enumerate(range(lo, hi)):
+        out[k] = W.make_image(c["rows"], c["cols"], c["shapes"], c["sigma"], seed=1 * 1000003 + b,
+                              quantize=c.get("quantize", False))
+    return out
+
+
+def describe(cfg_name, c, S, K, h, n_items):
+    if c["kind"] == "signal":
+        wl = f"{cfg_name}: 1D PatchLift NLM, N={c['n']} fp32 piecewise-constant+noise"
+        return {"workload": wl, "n": c["n"], "S": S, "K": K, "h": round(h, 4), "order": "1d"}
+    wl = (f"{cfg_name}: {c['batch']} x {c['rows']}x{c['cols']} "
+          f"{'integer-valued (quantised) ' if c.get('quantize') else ''}fp32 synthetic images, "
+          f"{c['shapes']} shapes, sigma={c['sigma']}")
+    return {"workload": wl, "images": n_items, "rows": c["rows"], "cols": c["cols"], "S": S, "K": K,
+            "h": round(h, 4), "order": "row->col (snlm_2d_row_col)"}
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------- peaks
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f)
+    return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "fallback": True}
+
+
+def mufu_peak():
+    """Live MUFU.EX2 throughput (exps/s) from lib/libplubench.so, full chip."""
+    import ctypes as C
+    so = os.path.join(ROOT, "paper_1407_2343_b200", "lib", "libplubench.so")
+    if not os.path.exists(so):
+        return None, None
+    L = C.CDLL(so)
+    L.plub_rate.restype = C.c_double
+    L.plub_rate.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]
+    ms = C.c_double(0)
+    ex2 = L.plub_rate(0, 8, 256, 4096, C.byref(ms))
+    ffma = L.plub_rate(1, 8, 256, 4096, C.byref(ms))
+    return (ex2 if ex2 > 0 else None), (ffma if ffma > 0 else None)
+
+
+def ncu_traffic(cfg_name):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(p):
+        try:
+            with open(p) as f:
+                return json.load(f).get(cfg_name)
+        except (OSError, ValueError):
+            return None
+    return None
+
+
+# --------------------------------------------------------------------------- cpu
+def cpu_reference_rate(cfg_name, imgs_host, S, K, h, seconds, max_items=None):
+    """Reference library (oracle/_ref) RC on the host, all hardware threads.
+    Returns (Mpx/s, cores, sample description, kind)."""
+    from oracle import Oracle, Reference
+    if Reference.available():
+        eng, kind = Reference.get(), "reference"
+        cores = eng.hardware_concurrency()
+    else:
+        eng, kind = Oracle.get(), "port"
+        cores = os.cpu_count() or 1
+    c, *_ = workload(cfg_name)
+    done_px, t_total, n = 0, 0.0, 0
+    limit = max_items or imgs_host.shape[0]
+    while n < limit and (t_total < seconds or n == 0):
+        img = imgs_host[n % imgs_host.shape[0]].astype(np.float64)
+        t0 = time.perf_counter()
+        if c["kind"] == "signal":
+            eng.nlm_1d(img, S, K, h)
+        elif kind == "reference":
+            eng.filter("rc", img, S, K, h, threads=0)
+        else:
+            eng.snlm_rc(img, S, K, h, threads=cores)
+        t_total += time.perf_counter() - t0
+        done_px += img.size
+        n += 1
+    sample = (f"{n} of the workload's {c.get('batch', 1)} item(s) ({imgs_host.shape[-2] if imgs_host.ndim > 1 else 1}"
+              f"x{imgs_host.shape[-1]}), snlm_2d_row_col(threads=0) of the reference library, "
+              f"{t_total:.1f} s")
+    return done_px / t_total / 1e6, cores, sample, kind
+
+
+def run_reference_arm(args):
+    world, rank, local = dist_env()
+    c, S, K, h = workload(args.config)
+    n_items = c.get("batch", 1)
+    cfg = describe(args.config, c, S, K, h, n_items)
+    if rank != 0:
+        return
+    sample_imgs = make_inputs(args.config, 0, 1)
+    # each step: RC of one image of the workload (a bounded sample), all host threads
+    for _ in range(args.warmup):
+        cpu_reference_rate(args.config, sample_imgs, S, K, h, 0.0, max_items=1)
+    rates, cores, sample, kind = [], None, "", ""
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        r, cores, sample, kind = cpu_reference_rate(args.config, sample_imgs, S, K, h, 0.0,
+                                                    max_items=1)
+        rates.append(r)
+    wall = time.perf_counter() - t0
+    value = float(np.median(rates))
+    px = sample_imgs[0].size
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": px / value / 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded PCG64, see paper_1407_2343_b200/workloads.py)", "config": cfg,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+                         "sample": "each step: " + sample.split(",", 1)[1].strip()
+                         if "," in sample else sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "wall_s": wall,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- ours
+def run_ours(args):
+    import torch
+    import paper_1407_2343_b200 as pl
+
+    world, rank, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    c, S, K, h = workload(args.config)
+    params = (S, K, h)
+    n_items = c.get("batch", 1)
+    if c["kind"] == "signal":
+        lo, hi = 0, 1
+    else:
+        lo, hi = shard(n_items, world, rank)
+    imgs_host = make_inputs(args.config, lo, hi)
+    x = torch.from_numpy(imgs_host).to(dev)
+    y = torch.empty_like(x)
+    mid = torch.empty_like(x)
+    stream = torch.cuda.current_stream()
+    signal = c["kind"] == "signal"
+
+    def step():
+        if signal:
+            pl.nlm_1d_patchlift(x, params, out=y)
+            return
+        pl.nlm_row_pass(x, params, out=mid)
+        pl.nlm_col_pass(mid, params, out=y)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+
+    # per-launch timing of the two pass kernels (events on the launching stream)
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(dev.index) as clocks:
+        start.record(stream)
+        for k in range(args.steps):
+            ev[k][0].record(stream)
+            if signal:
+                pl.nlm_1d_patchlift(x, params, out=y)
+                ev[k][1].record(stream)
+            else:
+                pl.nlm_row_pass(x, params, out=mid)
+                ev[k][1].record(stream)
+                pl.nlm_col_pass(mid, params, out=y)
+            ev[k][2].record(stream)
+        end.record(stream)
+        torch.cuda.synchronize()
+        # keep sampling a short moment so very short regions still get clock samples
+        if len(clocks.lines) < 3:
+            time.sleep(0.35)
+    if world > 1:
+        torch.distributed.barrier()
+    ms_local = start.elapsed_time(end)
+    t = torch.tensor([ms_local], device=dev, dtype=torch.float64)
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    ms_total = float(t.item())
+    ms_step = ms_total / args.steps
+    row_ms = [ev[k][0].elapsed_time(ev[k][1]) for k in range(args.steps)]
+    col_ms = [ev[k][1].elapsed_time(ev[k][2]) for k in range(args.steps)]
+
+    if signal:
+        px_local = c["n"]
+        px_total = px_local
+    else:
+        px_local = (hi - lo) * c["rows"] * c["cols"]
+        px_total = n_items * c["rows"] * c["cols"]
+    value = px_total / (ms_step * 1e-3) / 1e6
+
+    # ---- roofline (dominant kernel): unique pairs = exps per launch ----------
+    if signal:
+        u_row = pl.unique_pairs(c["n"], S)
+        u_col = 0
+    else:
+        u_row = (hi - lo) * c["rows"] * pl.unique_pairs(c["cols"], S)
+        u_col = (hi - lo) * c["cols"] * pl.unique_pairs(c["rows"], S)
+    row_avg = float(np.mean(row_ms))
+    col_avg = float(np.mean(col_ms)) if not signal else 0.0
+    dom = "row" if row_avg * 1.0 >= col_avg else "col"
+    u_dom, t_dom = (u_row, row_avg) if dom == "row" else (u_col, col_avg)
+    peaks = measured_peaks()
+    ex2_peak, ffma_peak = (mufu_peak() if rank == 0 else (None, None))
+    f_max = peaks.get("sm_max_mhz", 1965.0) * 1e6
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    nominal = 16 * sms * f_max
+    achieved = u_dom / (t_dom * 1e-3)
+    peak = ex2_peak or nominal
+    hbm_bytes = 8 * px_local  # per pass: fp32 read + write
+    roof = {
+        "bound": "sfu", "achieved": achieved / 1e9, "peak": peak / 1e9, "unit": "Gexp/s",
+        "frac": achieved / peak, "traffic": ncu_traffic(args.config),
+        "kernel": f"nlm_pass_kernel ({dom} pass)",
+        "peak_source": "live MUFU.EX2 microbenchmark (lib/libplubench.so)" if ex2_peak
+        else f"nominal 16/clk/SM x {sms} SM x {f_max / 1e6:.0f} MHz",
+        "peak_nominal": nominal / 1e9,
+        "frac_of_nominal": achieved / nominal,
+        "algorithmic_per_launch": {"exps": u_dom, "hbm_bytes": hbm_bytes},
+        "row_pass_ms": row_avg, "col_pass_ms": col_avg,
+        "step_frac": (u_row + u_col) / (ms_step * 1e-3) / peak,
+        "hbm": {"achieved_gbs": hbm_bytes / (t_dom * 1e-3) / 1e9, "peak_gbs": peaks.get("hbm_gbs"),
+                "t_hbm_ms": hbm_bytes / (peaks.get("hbm_gbs", 6541.5) * 1e9) * 1e3},
+        "ffma_peak_gflops_measured": (ffma_peak / 1e9) if ffma_peak else None,
+    }
+
+    line = None
+    if rank == 0:
+        cfg = describe(args.config, c, S, K, h, n_items)
+        cfg["l2"] = ("inputs + intermediate exceed the 126 MB L2" if px_total * 4 > 126e6
+                     else "working set fits L2 (flush not applied; compute-bound kernel)")
+        cfg["parallelism"] = f"batch shards x{world}" if world > 1 else "1 GPU"
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded PCG64 constructions of BASELINE.json, "
+                    "paper_1407_2343_b200/workloads.py)",
+            "config": cfg, "roofline": roof, "clocks": clocks.summary(),
+            "gpu_launches": args.steps * (1 if signal else 2),
+        }
+
+    # ---- e2e through the C-ABI host entry point (N GPUs: each rank its shard) --
+    if not signal:
+        hin = torch.from_numpy(imgs_host).pin_memory()
+        hout = torch.empty_like(hin).pin_memory()
+        pl.snlm_2d_row_col_host(hin, params, hout)  # warm-up
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            pl.snlm_2d_row_col_host(hin, params, hout)
+        e2e_s = (time.perf_counter() - t0) / args.e2e_steps
+        te = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+        if world > 1:
+            torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
+        e2e_s = float(te.item())
+        ok = torch.equal(hout, y.cpu())
+        if rank == 0:
+            line["e2e"] = {"value": px_total / e2e_s / 1e6, "unit": UNIT,
+                           "h2d_bytes_per_step": int(hin.numel() * 4) * world,
+                           "d2h_bytes_per_step": int(hout.numel() * 4) * world,
+                           "api": "pl_snlm_2d_row_col_host (pinned host buffers)",
+                           "matches_device_result": bool(ok)}
+    elif rank == 0:
+        hin = torch.from_numpy(imgs_host).pin_memory()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            xd = hin.to(dev, non_blocking=True)
+            yd = pl.nlm_1d_patchlift(xd, params)
+            yh = yd.cpu()
+        e2e_s = (time.perf_counter() - t0) / args.e2e_steps
+        line["e2e"] = {"value": px_total / e2e_s / 1e6, "unit": UNIT,
+                       "h2d_bytes_per_step": int(hin.numel() * 4),
+                       "d2h_bytes_per_step": int(yh.numel() * 4)}
+
+    # ---- CPU baseline (rank 0, N=1 only) ----------------------------------------
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, cores, sample, kind = cpu_reference_rate(args.config, imgs_host, S, K, h,
+                                                    args.cpu_seconds)
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": kind,
+                                "sample": sample}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

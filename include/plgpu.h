@@ -1,0 +1,168 @@
+/* plgpu.h -- C ABI of the B200 PatchLift separable-NLM hot path.
+ *
+ * The reference (arXiv 1407.2343 artifact, C++20 library `patchlift`) has no
+ * FFI; its boundary is the C++ function API in proj/include/patchlift/.  This
+ * header is the flat, exception-free face of that API over DEVICE fp32
+ * buffers, one entry point per reference function it replaces:
+ *
+ *   pl_nlm_lines           nlm_1d_patchlift            nlm.hpp:30, nlm.cpp:144-166
+ *   pl_nlm_row_pass        nlm_row_pass                nlm.hpp:39-40, nlm.cpp:215-227
+ *   pl_nlm_col_pass        nlm_col_pass                nlm.hpp:41-42, nlm.cpp:229-232
+ *   pl_snlm_2d_row_col     snlm_2d_row_col             nlm.hpp:45-46, nlm.cpp:234-239
+ *   pl_snlm_2d_col_row     snlm_2d_col_row             nlm.hpp:47-48, nlm.cpp:241-246
+ *   pl_snlm_2d             snlm_2d (RC+CR)/2           nlm.hpp:51-52, nlm.cpp:248-253
+ *   pl_distance_band_f32   compute_banded_kernel + kernel_distance_sq over the
+ *   pl_distance_band_i32     band (BandedKernel cell layout)  banded_kernel.cpp:25-84
+ *   pl_banded_kernel_f64   compute_banded_kernel (F-bar values)  banded_kernel.cpp:25-72
+ *   pl_nlm_lines_naive     nlm_1d_naive (direct O(K) distances)  nlm.cpp:120-142
+ *   pl_validate_params     validate_params             core_types.cpp:49-69
+ *   pl_op_counts_1d        OpCounter closed forms      nlm.cpp:154-164, banded_kernel.cpp:49-66
+ *
+ * Conventions
+ *  - Buffers are caller-owned device pointers (fp32 unless stated); images
+ *    are batches of row-major [batch][rows][cols] planes.
+ *  - Every call is stream-ordered on `stream` (a cudaStream_t, NULL = legacy
+ *    default stream) and returns immediately; re-entrant per stream.
+ *  - Return value: PL_OK or an error code; the message of the last failure on
+ *    the calling thread is pl_last_error().  Validation failures reuse the
+ *    reference's exact ValidationError messages (core_types.cpp:13-77).
+ *  - Boundary convention: half-sample mirror for patch content
+ *    (core_types.cpp:71-88), search windows clipped to the line
+ *    (nlm.cpp:71-73).  S larger than line-1 behaves as line-1.
+ *  - Arithmetic: fp32 with IEEE division; weights exp(-d/h^2) evaluated as
+ *    ex2(d * c), c = -log2(e)/h^2 computed in double on the host.  Distances
+ *    are exact (bit-equal to the reference) on integer-valued inputs.
+ *  - Results are bitwise independent of batch size, line count, GPU count and
+ *    of which axis a line lies on (row and column passes run identical per-
+ *    line arithmetic), so transpose equivariance holds bit for bit.
+ */
+#ifndef PLGPU_H_
+#define PLGPU_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PLGPU_ABI_VERSION 1
+
+enum pl_status {
+  PL_OK = 0,
+  PL_ERR_VALIDATION = 1, /* reference ValidationError (std::invalid_argument) */
+  PL_ERR_RANGE = 2,      /* reference std::out_of_range */
+  PL_ERR_CUDA = 3,       /* CUDA runtime / launch failure */
+  PL_ERR_UNSUPPORTED = 4,
+  PL_ERR_ARG = 5 /* null pointer or malformed descriptor */
+};
+
+/* NlmParams (core_types.hpp:45-49): S, K, h. */
+typedef struct pl_params {
+  int32_t search_radius;
+  int32_t patch_radius;
+  double h;
+} pl_params;
+
+/* OpCounter (op_counter.hpp:9-24). */
+typedef struct pl_op_counts {
+  uint64_t adds;
+  uint64_t muls;
+  uint64_t exps;
+  uint64_t clamps;
+} pl_op_counts;
+
+int pl_abi_version(void);
+const char* pl_last_error(void);
+/* Name of the device the library will launch on, or "" if none. */
+const char* pl_device_name(void);
+
+/* Host-only checks with the reference's messages; no device is touched. */
+int pl_validate_params(pl_params p, int32_t n);
+int pl_validate_geometry(int32_t search_radius, int32_t patch_radius, int32_t n);
+
+/* Reference op-count closed forms for one 1D PatchLift filter of length n
+ * (kernel build + 4 adds, 2 muls, 1 exp per ordered window; clamps 0 because
+ * the squared-difference route is nonnegative by construction).  Added to
+ * *out. */
+int pl_op_counts_1d(int32_t n, pl_params p, pl_op_counts* out);
+
+/* Unique in-band pairs U(n,S) = n*S' - S'(S'+1)/2, S' = min(S, n-1): the exps
+ * the device evaluates per line (w_ij = w_ji, w_ii = 1). */
+uint64_t pl_unique_pairs(int32_t n, int32_t search_radius);
+
+/* Segment length the device uses for lines of length n (a function of n
+ * only, so results never depend on the launch shape). */
+int32_t pl_segment_length(int32_t n, int32_t search_radius);
+
+/* ---- 1D: n_lines lines of n samples, line l starts at src + l*ld ----- */
+int pl_nlm_lines(const float* src, float* dst, int64_t n_lines, int32_t n, int64_t ld,
+                 pl_params p, void* stream);
+int pl_nlm_lines_naive(const float* src, float* dst, int64_t n_lines, int32_t n, int64_t ld,
+                       pl_params p, void* stream);
+
+/* ---- 2D separable passes on [batch][rows][cols] ------------------------- */
+int pl_nlm_row_pass(const float* src, float* dst, int32_t batch, int32_t rows, int32_t cols,
+                    pl_params p, void* stream);
+int pl_nlm_col_pass(const float* src, float* dst, int32_t batch, int32_t rows, int32_t cols,
+                    pl_params p, void* stream);
+
+/* Row pass whose output is written in column blocks of width col_block:
+ * element (b, r, c) lands at dst + b*rows*cols + (c / col_block)*rows*col_block
+ * + r*col_block + (c % col_block).  With one image per rank this is exactly
+ * the send layout of the row-slab -> column-slab all-to-all (cols must be a
+ * multiple of col_block). */
+int pl_nlm_row_pass_blocked(const float* src, float* dst, int32_t batch, int32_t rows,
+                            int32_t cols, int32_t col_block, pl_params p, void* stream);
+
+/* Bytes of device workspace the composites need (0 for single passes). */
+size_t pl_workspace_bytes(int32_t op, int32_t batch, int32_t rows, int32_t cols);
+
+/* Composites.  `work` is caller-provided device scratch of
+ * pl_workspace_bytes(...) bytes, or NULL to use a library-owned cache. */
+int pl_snlm_2d_row_col(const float* src, float* dst, float* work, int32_t batch, int32_t rows,
+                       int32_t cols, pl_params p, void* stream);
+int pl_snlm_2d_col_row(const float* src, float* dst, float* work, int32_t batch, int32_t rows,
+                       int32_t cols, pl_params p, void* stream);
+int pl_snlm_2d(const float* src, float* dst, float* work, int32_t batch, int32_t rows,
+               int32_t cols, pl_params p, void* stream);
+
+/* End-to-end form of pl_snlm_2d_row_col over HOST buffers (pinned or
+ * pageable): the H2D copy, both passes and the D2H copy run on `stream`,
+ * chunked by image so copies overlap compute.  Blocks until done. */
+int pl_snlm_2d_row_col_host(const float* host_src, float* host_dst, int32_t batch, int32_t rows,
+                            int32_t cols, pl_params p, void* stream);
+
+/* ---- classical 2D NLM (nlm_2d_naive, nlm.cpp:168-213): the baseline the
+ * separable filter is compared against (per-pixel (2S+1)^2 window, direct
+ * (2K+1)^2 patch distances, 2D half-sample mirror).  Not the hot path. */
+int pl_nlm_2d_naive(const float* src, float* dst, int32_t batch, int32_t rows, int32_t cols,
+                    pl_params p, void* stream);
+
+/* ---- device memory helpers so host layers need no CUDA runtime of their own */
+int pl_device_alloc(void** ptr, size_t bytes);
+int pl_device_free(void* ptr);
+int pl_copy_to_device(void* dst, const void* src, size_t bytes);
+int pl_copy_to_host(void* dst, const void* src, size_t bytes);
+int pl_synchronize(void);
+
+/* ---- distance / kernel bands (BandedKernel layout, banded_kernel.hpp:11-38)
+ * band[l][i][o] for pair (i, i+o-S), o in [0, 2S+1); cells whose partner is
+ * outside [0,n) hold the sentinel NaN (f32/f64) or -1 (i32). */
+int pl_distance_band_f32(const float* src, float* band, int64_t n_lines, int32_t n, int64_t ld,
+                         int32_t search_radius, int32_t patch_radius, void* stream);
+/* Integer distances; src must hold integer values (|x| <= 2^24 / ...).  The
+ * device computes them exactly in the same running-sum recurrence as the
+ * filter and converts to int32. */
+int pl_distance_band_i32(const float* src, int32_t* band, int64_t n_lines, int32_t n, int64_t ld,
+                         int32_t search_radius, int32_t patch_radius, void* stream);
+/* F-bar cells of compute_banded_kernel in fp64, same diagonal recursion and
+ * evaluation order as the reference (bit-equal to it). src is fp64. */
+int pl_banded_kernel_f64(const double* src, double* band, int64_t n_lines, int32_t n, int64_t ld,
+                         int32_t search_radius, int32_t patch_radius, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PLGPU_H_ */

@@ -1,0 +1,311 @@
+"""paper_1407_2343_b200 -- B200-native PatchLift separable-NLM hot path.
+
+Python face of the C ABI in ``include/plgpu.h`` (``lib/libplgpu.so``), used by
+the tests and by ``bench.py``.  Device buffers are torch CUDA tensors (torch is
+plumbing here: allocation, streams, ``torch.distributed``); every filter runs
+in the hand-written sm_100a kernels behind the C ABI.  There is no CPU route:
+if the native library is missing, :func:`lib` raises.
+
+Names mirror the reference API (``proj/include/patchlift/nlm.hpp``):
+``nlm_1d_patchlift`` (batched lines), ``nlm_row_pass``, ``nlm_col_pass``,
+``snlm_2d_row_col``, ``snlm_2d_col_row``, ``snlm_2d``, plus the distance-band
+and F-bar exports of ``banded_kernel.hpp``.  Errors raise :class:`ValidationError`
+with the reference's messages.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import os
+from dataclasses import dataclass
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIBDIR = os.path.join(PKG, "lib")
+LIBPLGPU = os.path.join(LIBDIR, "libplgpu.so")
+LIBDROPIN = os.path.join(LIBDIR, "libpatchlift_b200.so")
+
+PL_OK, PL_ERR_VALIDATION, PL_ERR_RANGE, PL_ERR_CUDA, PL_ERR_UNSUPPORTED, PL_ERR_ARG = range(6)
+
+# Every symbol include/plgpu.h declares (checked by tests/test_capi.py).
+EXPORTS = [
+    "pl_abi_version", "pl_last_error", "pl_device_name", "pl_validate_params",
+    "pl_validate_geometry", "pl_op_counts_1d", "pl_unique_pairs", "pl_segment_length",
+    "pl_nlm_lines", "pl_nlm_lines_naive", "pl_nlm_row_pass", "pl_nlm_col_pass",
+    "pl_nlm_row_pass_blocked", "pl_workspace_bytes", "pl_snlm_2d_row_col",
+    "pl_snlm_2d_col_row", "pl_snlm_2d", "pl_snlm_2d_row_col_host", "pl_nlm_2d_naive",
+    "pl_device_alloc", "pl_device_free", "pl_copy_to_device", "pl_copy_to_host",
+    "pl_synchronize", "pl_distance_band_f32", "pl_distance_band_i32", "pl_banded_kernel_f64",
+]
+
+
+class ValidationError(ValueError):
+    """The reference's ``patchlift::ValidationError`` (a std::invalid_argument)."""
+
+
+class DeviceError(RuntimeError):
+    """CUDA failure inside the native library."""
+
+
+class _Params(C.Structure):
+    _fields_ = [("search_radius", C.c_int32), ("patch_radius", C.c_int32), ("h", C.c_double)]
+
+
+class _OpCounts(C.Structure):
+    _fields_ = [("adds", C.c_uint64), ("muls", C.c_uint64), ("exps", C.c_uint64),
+                ("clamps", C.c_uint64)]
+
+
+@dataclass
+class NlmParams:
+    """``NlmParams`` (core_types.hpp:45-49)."""
+
+    search_radius: int = 10
+    patch_radius: int = 3
+    h: float = 0.0
+
+    def c(self) -> _Params:
+        return _Params(int(self.search_radius), int(self.patch_radius), float(self.h))
+
+
+_LIB = None
+
+
+def lib() -> C.CDLL:
+    """Load ``lib/libplgpu.so`` (build it with ``__graft_entry__.build()``)."""
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(LIBPLGPU):
+            raise ImportError(f"native library missing: {LIBPLGPU}; run __graft_entry__.build()")
+        L = C.CDLL(LIBPLGPU)
+        vp, i32, i64 = C.c_void_p, C.c_int32, C.c_int64
+        P = _Params
+        sig = {
+            "pl_abi_version": ([], C.c_int),
+            "pl_last_error": ([], C.c_char_p),
+            "pl_device_name": ([], C.c_char_p),
+            "pl_validate_params": ([P, i32], C.c_int),
+            "pl_validate_geometry": ([i32, i32, i32], C.c_int),
+            "pl_op_counts_1d": ([i32, P, C.POINTER(_OpCounts)], C.c_int),
+            "pl_unique_pairs": ([i32, i32], C.c_uint64),
+            "pl_segment_length": ([i32, i32], i32),
+            "pl_nlm_lines": ([vp, vp, i64, i32, i64, P, vp], C.c_int),
+            "pl_nlm_lines_naive": ([vp, vp, i64, i32, i64, P, vp], C.c_int),
+            "pl_nlm_row_pass": ([vp, vp, i32, i32, i32, P, vp], C.c_int),
+            "pl_nlm_col_pass": ([vp, vp, i32, i32, i32, P, vp], C.c_int),
+            "pl_nlm_row_pass_blocked": ([vp, vp, i32, i32, i32, i32, P, vp], C.c_int),
+            "pl_workspace_bytes": ([i32, i32, i32, i32], C.c_size_t),
+            "pl_snlm_2d_row_col": ([vp, vp, vp, i32, i32, i32, P, vp], C.c_int),
+            "pl_snlm_2d_col_row": ([vp, vp, vp, i32, i32, i32, P, vp], C.c_int),
+            "pl_snlm_2d": ([vp, vp, vp, i32, i32, i32, P, vp], C.c_int),
+            "pl_snlm_2d_row_col_host": ([vp, vp, i32, i32, i32, P, vp], C.c_int),
+            "pl_nlm_2d_naive": ([vp, vp, i32, i32, i32, P, vp], C.c_int),
+            "pl_distance_band_f32": ([vp, vp, i64, i32, i64, i32, i32, vp], C.c_int),
+            "pl_distance_band_i32": ([vp, vp, i64, i32, i64, i32, i32, vp], C.c_int),
+            "pl_banded_kernel_f64": ([vp, vp, i64, i32, i64, i32, i32, vp], C.c_int),
+        }
+        for name, (args, res) in sig.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = res
+        _LIB = L
+    return _LIB
+
+
+def _check(rc: int) -> None:
+    if rc == PL_OK:
+        return
+    msg = (lib().pl_last_error() or b"").decode()
+    if rc == PL_ERR_VALIDATION:
+        raise ValidationError(msg)
+    if rc == PL_ERR_RANGE:
+        raise IndexError(msg)
+    if rc == PL_ERR_CUDA:
+        raise DeviceError(msg)
+    raise RuntimeError(f"plgpu error {rc}: {msg}")
+
+
+def _params(p) -> _Params:
+    if isinstance(p, NlmParams):
+        return p.c()
+    S, K, h = p
+    return _Params(int(S), int(K), float(h))
+
+
+def _stream(t) -> int:
+    import torch
+    return torch.cuda.current_stream(t.device).cuda_stream
+
+
+def _dev(t, dtype=None):
+    import torch
+    if not (isinstance(t, torch.Tensor) and t.is_cuda):
+        raise TypeError("expected a CUDA tensor")
+    if dtype is not None and t.dtype != dtype:
+        raise TypeError(f"expected dtype {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError("expected a contiguous tensor")
+    return t
+
+
+# ---------------------------------------------------------------------------
+# host-side helpers (no device)
+def validate_params(p, n: int) -> None:
+    _check(lib().pl_validate_params(_params(p), int(n)))
+
+
+def validate_geometry(S: int, K: int, n: int) -> None:
+    _check(lib().pl_validate_geometry(int(S), int(K), int(n)))
+
+
+def op_counts_1d(n: int, p) -> dict:
+    o = _OpCounts(0, 0, 0, 0)
+    _check(lib().pl_op_counts_1d(int(n), _params(p), C.byref(o)))
+    return {"adds": o.adds, "muls": o.muls, "exps": o.exps, "clamps": o.clamps}
+
+
+def unique_pairs(n: int, S: int) -> int:
+    return int(lib().pl_unique_pairs(int(n), int(S)))
+
+
+def segment_length(n: int, S: int) -> int:
+    return int(lib().pl_segment_length(int(n), int(S)))
+
+
+def weight_coef(h: float) -> float:
+    """c = -log2(e)/h^2 as the device uses it (w = 2^(c d))."""
+    return -1.4426950408889634 / (h * h)
+
+
+# ---------------------------------------------------------------------------
+# device filters over torch CUDA tensors (float32, contiguous)
+def _image_dims(x):
+    if x.dim() == 2:
+        return 1, x.shape[0], x.shape[1]
+    if x.dim() == 3:
+        return x.shape[0], x.shape[1], x.shape[2]
+    raise ValueError("expected [rows, cols] or [batch, rows, cols]")
+
+
+def nlm_1d_patchlift(x, p, out=None):
+    """1D PatchLift NLM on every line of ``x`` ([n] or [lines, n])."""
+    import torch
+    _dev(x, torch.float32)
+    n = x.shape[-1]
+    lines = x.numel() // n if n else 0
+    out = torch.empty_like(x) if out is None else out
+    _check(lib().pl_nlm_lines(x.data_ptr(), out.data_ptr(), lines, n, n, _params(p), _stream(x)))
+    return out
+
+
+def nlm_1d_naive(x, p, out=None):
+    import torch
+    _dev(x, torch.float32)
+    n = x.shape[-1]
+    out = torch.empty_like(x) if out is None else out
+    _check(lib().pl_nlm_lines_naive(x.data_ptr(), out.data_ptr(), x.numel() // n, n, n,
+                                    _params(p), _stream(x)))
+    return out
+
+
+def _image_op(name, x, p, out=None, work=None):
+    import torch
+    _dev(x, torch.float32)
+    b, r, c = _image_dims(x)
+    out = torch.empty_like(x) if out is None else out
+    fn = getattr(lib(), name)
+    if name in ("pl_nlm_row_pass", "pl_nlm_col_pass", "pl_nlm_2d_naive"):
+        rc = fn(x.data_ptr(), out.data_ptr(), b, r, c, _params(p), _stream(x))
+    else:
+        rc = fn(x.data_ptr(), out.data_ptr(), None if work is None else work.data_ptr(), b, r, c,
+                _params(p), _stream(x))
+    _check(rc)
+    return out
+
+
+def nlm_row_pass(x, p, out=None):
+    return _image_op("pl_nlm_row_pass", x, p, out)
+
+
+def nlm_col_pass(x, p, out=None):
+    return _image_op("pl_nlm_col_pass", x, p, out)
+
+
+def snlm_2d_row_col(x, p, out=None, work=None):
+    return _image_op("pl_snlm_2d_row_col", x, p, out, work)
+
+
+def snlm_2d_col_row(x, p, out=None, work=None):
+    return _image_op("pl_snlm_2d_col_row", x, p, out, work)
+
+
+def snlm_2d(x, p, out=None, work=None):
+    return _image_op("pl_snlm_2d", x, p, out, work)
+
+
+def nlm_2d_naive(x, p, out=None):
+    return _image_op("pl_nlm_2d_naive", x, p, out)
+
+
+def nlm_row_pass_blocked(x, p, col_block: int, out=None):
+    """Row pass writing [col_block]-wide column blocks (the all-to-all send layout)."""
+    import torch
+    _dev(x, torch.float32)
+    b, r, c = _image_dims(x)
+    out = torch.empty_like(x) if out is None else out
+    _check(lib().pl_nlm_row_pass_blocked(x.data_ptr(), out.data_ptr(), b, r, c, int(col_block),
+                                         _params(p), _stream(x)))
+    return out
+
+
+def workspace_bytes(op: int, batch: int, rows: int, cols: int) -> int:
+    return int(lib().pl_workspace_bytes(op, batch, rows, cols))
+
+
+def snlm_2d_row_col_host(x_host, p, out_host=None):
+    """End-to-end RC over HOST float32 arrays/tensors (copies inside)."""
+    import numpy as np
+    import torch
+    if isinstance(x_host, torch.Tensor):
+        assert not x_host.is_cuda and x_host.dtype == torch.float32 and x_host.is_contiguous()
+        src = x_host.data_ptr()
+        out_host = torch.empty_like(x_host) if out_host is None else out_host
+        dst = out_host.data_ptr()
+        shape = tuple(x_host.shape)
+    else:
+        x_host = np.ascontiguousarray(x_host, dtype=np.float32)
+        out_host = np.empty_like(x_host) if out_host is None else out_host
+        src, dst, shape = x_host.ctypes.data, out_host.ctypes.data, x_host.shape
+    b, r, c = (1,) + shape if len(shape) == 2 else shape
+    stream = torch.cuda.current_stream().cuda_stream
+    _check(lib().pl_snlm_2d_row_col_host(src, dst, b, r, c, _params(p), stream))
+    return out_host
+
+
+def distance_band(x, S: int, K: int, dtype=None):
+    """Distance band [lines, n, 2S+1] (NaN / -1 outside the line), int32 or fp32."""
+    import torch
+    _dev(x, torch.float32)
+    dtype = dtype or torch.float32
+    n = x.shape[-1]
+    lines = x.numel() // n
+    band = torch.empty((lines, n, 2 * S + 1), dtype=dtype, device=x.device)
+    fn = lib().pl_distance_band_i32 if dtype == torch.int32 else lib().pl_distance_band_f32
+    _check(fn(x.data_ptr(), band.data_ptr(), lines, n, n, int(S), int(K), _stream(x)))
+    return band
+
+
+def banded_kernel_f64(x, S: int, K: int):
+    """F-bar band [lines, n, 2S+1] in fp64 (compute_banded_kernel)."""
+    import torch
+    _dev(x, torch.float64)
+    n = x.shape[-1]
+    lines = x.numel() // n
+    band = torch.empty((lines, n, 2 * S + 1), dtype=torch.float64, device=x.device)
+    _check(lib().pl_banded_kernel_f64(x.data_ptr(), band.data_ptr(), lines, n, n, int(S), int(K),
+                                      _stream(x)))
+    return band
+
+
+def h_for(sigma: float, K: int) -> float:
+    """The configs' rule h = sqrt(2(2K+1)) * sigma."""
+    return math.sqrt(2 * (2 * K + 1)) * sigma

@@ -1,0 +1,520 @@
+// plgpu.cu -- C ABI (include/plgpu.h) over the sm_100a PatchLift kernels.
+// Host-side responsibilities: the reference's validation (core_types.cpp:49-69,
+// same messages), effective radius clipping, segment geometry, dispatch onto
+// the S-specialised walker instantiations, and composite sequencing.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "plgpu.h"
+#include "plgpu_aux.cuh"
+#include "plgpu_launch.cuh"
+#include "plgpu_walk.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+int set_err(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define PL_CUDA(expr)                                                              \
+  do {                                                                             \
+    cudaError_t e_ = (expr);                                                       \
+    if (e_ != cudaSuccess)                                                         \
+      return set_err(PL_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+int check_launch() {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_err(PL_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
+  return PL_OK;
+}
+
+// validate_geometry / validate_params (core_types.cpp:49-69).
+int validate_geometry(int S, int K, int n) {
+  if (n < 1) return set_err(PL_ERR_VALIDATION, "signal length must be at least 1");
+  if (S < 0) return set_err(PL_ERR_VALIDATION, "search radius must be nonnegative");
+  if (K < 0) return set_err(PL_ERR_VALIDATION, "patch radius must be nonnegative");
+  if (K > n) return set_err(PL_ERR_VALIDATION, "patch radius exceeds signal length");
+  return PL_OK;
+}
+
+int validate_params(const pl_params& p, int n) {
+  int rc = validate_geometry(p.search_radius, p.patch_radius, n);
+  if (rc) return rc;
+  if (!(p.h > 0.0)) return set_err(PL_ERR_VALIDATION, "smoothing parameter h must be positive");
+  return PL_OK;
+}
+
+int validate_image(int batch, int rows, int cols) {
+  if (rows < 1 || cols < 1) return set_err(PL_ERR_VALIDATION, "image dimensions must be at least 1x1");
+  if (batch < 1) return set_err(PL_ERR_ARG, "batch must be at least 1");
+  return PL_OK;
+}
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Segment length: a function of the line length (and S) only.
+int32_t segment_length(int32_t n, int32_t S) {
+  (void)S;
+  const int32_t C = 128;
+  return n < C ? n : C;
+}
+
+// Largest radius with a specialised walker; larger radii use the direct kernel.
+constexpr int kMaxWalkS = 32;
+// Instantiated template radii; an effective S runs on the smallest >= it
+// (extra offsets are masked to weight exactly 0, which leaves every sum
+// bitwise unchanged).
+constexpr int kWalkS[] = {1, 2, 3, 4, 5, 6, 7, 8, 10, 12, 15, 16, 20, 25, 32};
+
+int template_radius(int S) {
+  for (int t : kWalkS)
+    if (t >= S) return t;
+  return -1;
+}
+
+int dispatch_pass(const plgpu::PassDesc& g, cudaStream_t st) {
+  switch (template_radius(g.S)) {
+#define PL_CASE(v) \
+  case v: plgpu::launch_pass<v>(g, st); break;
+    PLGPU_FOR_EACH_RADIUS(PL_CASE)
+#undef PL_CASE
+    default:
+      return set_err(PL_ERR_UNSUPPORTED, "search radius above walker range");
+  }
+  return check_launch();
+}
+
+float weight_coef(double h) { return static_cast<float>(-1.4426950408889634 / (h * h)); }
+
+// Generic direct-route pass over strided lines (used for S > kMaxWalkS and S == 0).
+__global__ void direct_pass_kernel(plgpu::PassDesc g) {
+  const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= g.n_lines * g.n) return;
+  const int64_t line = w % g.n_lines;
+  const int i = (int)(w / g.n_lines);
+  const int64_t img = line / g.lines_per_img;
+  const int64_t li = line - img * g.lines_per_img;
+  const float* f = g.src + img * g.src_img_stride + li * g.src_line_stride;
+  const int64_t ps = g.src_pos_stride;
+  const int n = g.n, K = g.K;
+  const int lo = max(0, i - g.S), hi = min(n - 1, i + g.S);
+  float num = 0.f, den = 0.f;
+  for (int j = lo; j <= hi; ++j) {
+    float dsq = 0.f;
+    for (int t = -K; t <= K; ++t) {
+      const float df = __ldg(f + plgpu::mirror_pos(i + t, n) * ps) -
+                       __ldg(f + plgpu::mirror_pos(j + t, n) * ps);
+      dsq = fmaf(df, df, dsq);
+    }
+    const float wt = (j == i) ? 1.f : plgpu::ex2_approx(g.coef * dsq);
+    num = fmaf(wt, __ldg(f + (int64_t)j * ps), num);
+    den += wt;
+  }
+  const int blk = g.dst_pos_block;
+  float* dst = g.dst + img * g.dst_img_stride + li * g.dst_line_stride +
+               (int64_t)(i / blk) * g.dst_block_stride + (int64_t)(i % blk) * g.dst_pos_stride;
+  *dst = num / den;
+}
+
+int run_pass(plgpu::PassDesc g, const pl_params& p, cudaStream_t st) {
+  g.S = std::min<int32_t>(p.search_radius, g.n - 1);
+  g.K = p.patch_radius;
+  g.coef = weight_coef(p.h);
+  g.seg_len = segment_length(g.n, g.S);
+  g.nseg = (g.n + g.seg_len - 1) / g.seg_len;
+  if (g.dst_pos_block <= 0) g.dst_pos_block = g.n;
+  if (g.n_lines <= 0) return PL_OK;
+  if (g.S >= 1 && g.S <= kMaxWalkS) return dispatch_pass(g, st);
+  const int64_t work = g.n_lines * g.n;
+  direct_pass_kernel<<<(unsigned)((work + 127) / 128), 128, 0, st>>>(g);
+  return check_launch();
+}
+
+plgpu::PassDesc row_desc(const float* src, float* dst, int batch, int rows, int cols) {
+  plgpu::PassDesc g{};
+  g.src = src;
+  g.dst = dst;
+  g.n_lines = (int64_t)batch * rows;
+  g.lines_per_img = rows;
+  g.src_img_stride = g.dst_img_stride = (int64_t)rows * cols;
+  g.src_line_stride = g.dst_line_stride = cols;
+  g.src_pos_stride = g.dst_pos_stride = 1;
+  g.dst_block_stride = 0;
+  g.dst_pos_block = cols;
+  g.n = cols;
+  return g;
+}
+
+plgpu::PassDesc col_desc(const float* src, float* dst, int batch, int rows, int cols) {
+  plgpu::PassDesc g{};
+  g.src = src;
+  g.dst = dst;
+  g.n_lines = (int64_t)batch * cols;
+  g.lines_per_img = cols;
+  g.src_img_stride = g.dst_img_stride = (int64_t)rows * cols;
+  g.src_line_stride = g.dst_line_stride = 1;
+  g.src_pos_stride = g.dst_pos_stride = cols;
+  g.dst_block_stride = 0;
+  g.dst_pos_block = rows;
+  g.n = rows;
+  return g;
+}
+
+// Library-owned workspace cache (per device, grown on demand, stream-ordered use).
+struct Workspace {
+  std::mutex mu;
+  void* ptr = nullptr;
+  size_t bytes = 0;
+};
+Workspace g_ws[64];
+
+int get_workspace(size_t bytes, float** out) {
+  int dev = 0;
+  PL_CUDA(cudaGetDevice(&dev));
+  Workspace& ws = g_ws[dev & 63];
+  std::lock_guard<std::mutex> lk(ws.mu);
+  if (ws.bytes < bytes) {
+    if (ws.ptr) {
+      PL_CUDA(cudaDeviceSynchronize());
+      PL_CUDA(cudaFree(ws.ptr));
+      ws.ptr = nullptr;
+      ws.bytes = 0;
+    }
+    PL_CUDA(cudaMalloc(&ws.ptr, bytes));
+    ws.bytes = bytes;
+  }
+  *out = static_cast<float*>(ws.ptr);
+  return PL_OK;
+}
+
+int check_ptrs(const void* a, const void* b) {
+  if (!a || !b) return set_err(PL_ERR_ARG, "null buffer");
+  return PL_OK;
+}
+
+}  // namespace
+
+namespace {
+template <typename T>
+int distance_band(const float* src, T* band, int64_t n_lines, int32_t n, int64_t ld, int32_t S,
+                  int32_t K, cudaStream_t st) {
+  int rc = validate_geometry(S, K, n);
+  if (rc) return rc;
+  if ((rc = check_ptrs(src, band))) return rc;
+  if (n_lines <= 0) return PL_OK;
+  const int64_t cells = n_lines * (int64_t)n * (2 * S + 1);
+  PL_CUDA(cudaMemsetAsync(band, 0xFF, cells * sizeof(T), st));  // NaN / -1 sentinel
+  plgpu::BandDesc g{};
+  g.src = src;
+  g.band = band;
+  g.n_lines = n_lines;
+  g.ld = ld;
+  g.n = n;
+  g.S = std::min<int32_t>(S, n - 1);
+  g.S_band = S;
+  g.K = K;
+  g.seg_len = segment_length(n, g.S);
+  g.nseg = (n + g.seg_len - 1) / g.seg_len;
+  if (g.S > kMaxWalkS) {
+    const int64_t work = n_lines * (int64_t)n;
+    plgpu::distance_band_direct_kernel<T><<<(unsigned)((work + 127) / 128), 128, 0, st>>>(g);
+    return check_launch();
+  }
+  switch (template_radius(std::max(1, g.S))) {
+#define PL_CASE(v) \
+  case v: plgpu::launch_band<v, T>(g, st); break;
+    PLGPU_FOR_EACH_RADIUS(PL_CASE)
+#undef PL_CASE
+    default:
+      return set_err(PL_ERR_UNSUPPORTED, "search radius above walker range");
+  }
+  return check_launch();
+}
+}  // namespace
+
+extern "C" {
+
+int pl_abi_version(void) { return PLGPU_ABI_VERSION; }
+
+const char* pl_last_error(void) { return g_err.c_str(); }
+
+const char* pl_device_name(void) {
+  static thread_local char name[256];
+  name[0] = 0;
+  int dev = 0;
+  cudaDeviceProp prop;
+  if (cudaGetDevice(&dev) == cudaSuccess && cudaGetDeviceProperties(&prop, dev) == cudaSuccess)
+    std::snprintf(name, sizeof(name), "%s", prop.name);
+  else
+    cudaGetLastError();
+  return name;
+}
+
+int pl_validate_params(pl_params p, int32_t n) { return validate_params(p, n); }
+
+int pl_validate_geometry(int32_t S, int32_t K, int32_t n) { return validate_geometry(S, K, n); }
+
+int pl_op_counts_1d(int32_t n, pl_params p, pl_op_counts* out) {
+  int rc = validate_params(p, n);
+  if (rc) return rc;
+  if (!out) return set_err(PL_ERR_ARG, "null op counter");
+  const uint64_t S = (uint64_t)p.search_radius, K = (uint64_t)p.patch_radius;
+  // compute_banded_kernel (banded_kernel.cpp:49-66): per diagonal d <= min(S, n-1)
+  const int64_t maxd = std::min<int64_t>(p.search_radius, (int64_t)n - 1);
+  uint64_t adds = 0, muls = 0, windows = 0;
+  for (int64_t d = 0; d <= maxd; ++d) {
+    adds += 2 * K + 2 * (uint64_t)(n - d - 1);
+    muls += 2 * K + 1 + 2 * (uint64_t)(n - d - 1);
+  }
+  // window loop (nlm.cpp:155-162)
+  for (int64_t i = 0; i < n; ++i) {
+    const int64_t lo = std::max<int64_t>(0, i - (int64_t)S);
+    const int64_t hi = std::min<int64_t>(n - 1, i + (int64_t)S);
+    windows += (uint64_t)(hi - lo + 1);
+  }
+  out->adds += adds + windows * 4;
+  out->muls += muls + windows * 2;
+  out->exps += windows;
+  return PL_OK;
+}
+
+uint64_t pl_unique_pairs(int32_t n, int32_t S) {
+  if (n < 1 || S < 0) return 0;
+  const uint64_t s = (uint64_t)std::min<int64_t>(S, (int64_t)n - 1);
+  return (uint64_t)n * s - s * (s + 1) / 2;
+}
+
+int32_t pl_segment_length(int32_t n, int32_t S) { return segment_length(n, S); }
+
+int pl_nlm_lines(const float* src, float* dst, int64_t n_lines, int32_t n, int64_t ld, pl_params p,
+                 void* stream) {
+  int rc = validate_params(p, n);
+  if (rc) return rc;
+  if ((rc = check_ptrs(src, dst))) return rc;
+  plgpu::PassDesc g{};
+  g.src = src;
+  g.dst = dst;
+  g.n_lines = n_lines;
+  g.lines_per_img = (int32_t)std::max<int64_t>(1, std::min<int64_t>(n_lines, INT32_MAX));
+  g.src_img_stride = g.dst_img_stride = ld * g.lines_per_img;
+  g.src_line_stride = g.dst_line_stride = ld;
+  g.src_pos_stride = g.dst_pos_stride = 1;
+  g.dst_pos_block = n;
+  g.n = n;
+  return run_pass(g, p, as_stream(stream));
+}
+
+int pl_nlm_lines_naive(const float* src, float* dst, int64_t n_lines, int32_t n, int64_t ld,
+                       pl_params p, void* stream) {
+  int rc = validate_params(p, n);
+  if (rc) return rc;
+  if ((rc = check_ptrs(src, dst))) return rc;
+  if (n_lines <= 0) return PL_OK;
+  plgpu::DirectDesc g{src, dst, n_lines, ld, n, p.search_radius, p.patch_radius,
+                      weight_coef(p.h)};
+  const int64_t work = n_lines * n;
+  plgpu::nlm_direct_kernel<<<(unsigned)((work + 127) / 128), 128, 0, as_stream(stream)>>>(g);
+  return check_launch();
+}
+
+int pl_nlm_row_pass(const float* src, float* dst, int32_t batch, int32_t rows, int32_t cols,
+                    pl_params p, void* stream) {
+  int rc = validate_image(batch, rows, cols);
+  if (!rc) rc = validate_params(p, cols);
+  if (!rc) rc = check_ptrs(src, dst);
+  if (rc) return rc;
+  return run_pass(row_desc(src, dst, batch, rows, cols), p, as_stream(stream));
+}
+
+int pl_nlm_col_pass(const float* src, float* dst, int32_t batch, int32_t rows, int32_t cols,
+                    pl_params p, void* stream) {
+  int rc = validate_image(batch, rows, cols);
+  if (!rc) rc = validate_params(p, rows);
+  if (!rc) rc = check_ptrs(src, dst);
+  if (rc) return rc;
+  return run_pass(col_desc(src, dst, batch, rows, cols), p, as_stream(stream));
+}
+
+int pl_nlm_row_pass_blocked(const float* src, float* dst, int32_t batch, int32_t rows,
+                            int32_t cols, int32_t col_block, pl_params p, void* stream) {
+  int rc = validate_image(batch, rows, cols);
+  if (!rc) rc = validate_params(p, cols);
+  if (!rc) rc = check_ptrs(src, dst);
+  if (rc) return rc;
+  if (col_block < 1 || cols % col_block != 0)
+    return set_err(PL_ERR_ARG, "cols must be a positive multiple of col_block");
+  plgpu::PassDesc g = row_desc(src, dst, batch, rows, cols);
+  g.dst_line_stride = col_block;
+  g.dst_pos_block = col_block;
+  g.dst_block_stride = (int64_t)rows * col_block;
+  return run_pass(g, p, as_stream(stream));
+}
+
+size_t pl_workspace_bytes(int32_t op, int32_t batch, int32_t rows, int32_t cols) {
+  const size_t img = (size_t)std::max(batch, 0) * std::max(rows, 0) * std::max(cols, 0) * sizeof(float);
+  return op == 2 ? 3 * img : img;  // op 2: snlm (RC, CR, mid); else one intermediate
+}
+
+int pl_snlm_2d_row_col(const float* src, float* dst, float* work, int32_t batch, int32_t rows,
+                       int32_t cols, pl_params p, void* stream) {
+  int rc = validate_image(batch, rows, cols);
+  if (!rc) rc = validate_params(p, rows);
+  if (!rc) rc = validate_params(p, cols);
+  if (!rc) rc = check_ptrs(src, dst);
+  if (rc) return rc;
+  if (!work && (rc = get_workspace(pl_workspace_bytes(0, batch, rows, cols), &work))) return rc;
+  cudaStream_t st = as_stream(stream);
+  if ((rc = run_pass(row_desc(src, work, batch, rows, cols), p, st))) return rc;
+  return run_pass(col_desc(work, dst, batch, rows, cols), p, st);
+}
+
+int pl_snlm_2d_col_row(const float* src, float* dst, float* work, int32_t batch, int32_t rows,
+                       int32_t cols, pl_params p, void* stream) {
+  int rc = validate_image(batch, rows, cols);
+  if (!rc) rc = validate_params(p, rows);
+  if (!rc) rc = validate_params(p, cols);
+  if (!rc) rc = check_ptrs(src, dst);
+  if (rc) return rc;
+  if (!work && (rc = get_workspace(pl_workspace_bytes(1, batch, rows, cols), &work))) return rc;
+  cudaStream_t st = as_stream(stream);
+  if ((rc = run_pass(col_desc(src, work, batch, rows, cols), p, st))) return rc;
+  return run_pass(row_desc(work, dst, batch, rows, cols), p, st);
+}
+
+int pl_snlm_2d(const float* src, float* dst, float* work, int32_t batch, int32_t rows,
+               int32_t cols, pl_params p, void* stream) {
+  int rc = validate_image(batch, rows, cols);
+  if (!rc) rc = validate_params(p, rows);
+  if (!rc) rc = validate_params(p, cols);
+  if (!rc) rc = check_ptrs(src, dst);
+  if (rc) return rc;
+  if (!work && (rc = get_workspace(pl_workspace_bytes(2, batch, rows, cols), &work))) return rc;
+  const int64_t cnt = (int64_t)batch * rows * cols;
+  float* rc_img = work;
+  float* cr_img = work + cnt;
+  float* mid = work + 2 * cnt;
+  if ((rc = pl_snlm_2d_row_col(src, rc_img, mid, batch, rows, cols, p, stream))) return rc;
+  if ((rc = pl_snlm_2d_col_row(src, cr_img, mid, batch, rows, cols, p, stream))) return rc;
+  const int blocks = (int)std::min<int64_t>((cnt + 255) / 256, 148 * 16);
+  plgpu::average_kernel<<<blocks, 256, 0, as_stream(stream)>>>(rc_img, cr_img, dst, cnt);
+  return check_launch();
+}
+
+int pl_snlm_2d_row_col_host(const float* host_src, float* host_dst, int32_t batch, int32_t rows,
+                            int32_t cols, pl_params p, void* stream) {
+  int rc = validate_image(batch, rows, cols);
+  if (!rc) rc = validate_params(p, rows);
+  if (!rc) rc = validate_params(p, cols);
+  if (!rc) rc = check_ptrs(host_src, host_dst);
+  if (rc) return rc;
+  cudaStream_t st = as_stream(stream);
+  const size_t img = (size_t)rows * cols;
+  // Double-buffered per-image pipeline: H2D(b+1) overlaps compute(b) and D2H(b-1)
+  // through two streams.  Buffers: 2 x (in, mid, out).
+  float* buf = nullptr;
+  if ((rc = get_workspace(6 * img * sizeof(float), &buf))) return rc;
+  cudaStream_t s2 = nullptr;
+  PL_CUDA(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+  cudaStream_t sv[2] = {st, s2};
+  for (int b = 0; b < batch; ++b) {
+    cudaStream_t s = sv[b & 1];
+    float* in = buf + (size_t)(b & 1) * 3 * img;
+    float* mid = in + img;
+    float* out = mid + img;
+    PL_CUDA(cudaMemcpyAsync(in, host_src + (size_t)b * img, img * sizeof(float),
+                            cudaMemcpyHostToDevice, s));
+    if ((rc = run_pass(row_desc(in, mid, 1, rows, cols), p, s))) break;
+    if ((rc = run_pass(col_desc(mid, out, 1, rows, cols), p, s))) break;
+    PL_CUDA(cudaMemcpyAsync(host_dst + (size_t)b * img, out, img * sizeof(float),
+                            cudaMemcpyDeviceToHost, s));
+  }
+  cudaError_t e1 = cudaStreamSynchronize(s2);
+  cudaError_t e2 = cudaStreamSynchronize(st);
+  cudaStreamDestroy(s2);
+  if (rc) return rc;
+  if (e1 != cudaSuccess || e2 != cudaSuccess)
+    return set_err(PL_ERR_CUDA, std::string("host pipeline: ") +
+                                    cudaGetErrorString(e1 != cudaSuccess ? e1 : e2));
+  return PL_OK;
+}
+
+
+int pl_distance_band_f32(const float* src, float* band, int64_t n_lines, int32_t n, int64_t ld,
+                         int32_t S, int32_t K, void* stream) {
+  return distance_band<float>(src, band, n_lines, n, ld, S, K, as_stream(stream));
+}
+
+int pl_distance_band_i32(const float* src, int32_t* band, int64_t n_lines, int32_t n, int64_t ld,
+                         int32_t S, int32_t K, void* stream) {
+  return distance_band<int32_t>(src, band, n_lines, n, ld, S, K, as_stream(stream));
+}
+
+int pl_banded_kernel_f64(const double* src, double* band, int64_t n_lines, int32_t n, int64_t ld,
+                         int32_t S, int32_t K, void* stream) {
+  int rc = validate_geometry(S, K, n);
+  if (rc) return rc;
+  if ((rc = check_ptrs(src, band))) return rc;
+  if (n_lines <= 0) return PL_OK;
+  cudaStream_t st = as_stream(stream);
+  const int64_t cells = n_lines * (int64_t)n * (2 * S + 1);
+  PL_CUDA(cudaMemsetAsync(band, 0xFF, cells * sizeof(double), st));  // NaN sentinel
+  plgpu::KernelBandDesc g{src, band, n_lines, ld, n, std::min<int32_t>(S, n - 1), S, K};
+  const int64_t work = n_lines * (g.S + 1);
+  plgpu::banded_kernel_f64<<<(unsigned)((work + 127) / 128), 128, 0, st>>>(g);
+  return check_launch();
+}
+
+}  // extern "C"
+
+extern "C" {
+
+int pl_nlm_2d_naive(const float* src, float* dst, int32_t batch, int32_t rows, int32_t cols,
+                    pl_params p, void* stream) {
+  int rc = validate_image(batch, rows, cols);
+  if (!rc) rc = validate_params(p, std::min(rows, cols));
+  if (!rc) rc = check_ptrs(src, dst);
+  if (rc) return rc;
+  plgpu::Naive2DDesc g{src, dst, batch, rows, cols, p.search_radius, p.patch_radius,
+                       weight_coef(p.h)};
+  const int64_t work = (int64_t)batch * rows * cols;
+  plgpu::nlm_2d_naive_kernel<<<(unsigned)((work + 127) / 128), 128, 0, as_stream(stream)>>>(g);
+  return check_launch();
+}
+
+int pl_device_alloc(void** ptr, size_t bytes) {
+  if (!ptr) return set_err(PL_ERR_ARG, "null pointer");
+  PL_CUDA(cudaMalloc(ptr, bytes ? bytes : 1));
+  return PL_OK;
+}
+
+int pl_device_free(void* ptr) {
+  PL_CUDA(cudaFree(ptr));
+  return PL_OK;
+}
+
+int pl_copy_to_device(void* dst, const void* src, size_t bytes) {
+  PL_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice));
+  return PL_OK;
+}
+
+int pl_copy_to_host(void* dst, const void* src, size_t bytes) {
+  PL_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));
+  return PL_OK;
+}
+
+int pl_synchronize(void) {
+  PL_CUDA(cudaDeviceSynchronize());
+  return PL_OK;
+}
+
+}  // extern "C"

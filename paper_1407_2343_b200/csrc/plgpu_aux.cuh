@@ -1,0 +1,152 @@
+// plgpu_aux.cuh -- secondary device kernels behind the C ABI:
+//   * banded_kernel_f64: F-bar cells (compute_banded_kernel, banded_kernel.cpp:25-72)
+//     with the reference's own diagonal recursion and evaluation order in
+//     fp64 (explicit _rn intrinsics: no FMA contraction), so cells are
+//     bit-equal to the reference's.  Not on the filter's hot path.
+//   * nlm_direct_kernel: the direct O(K)-per-window route of nlm_1d_naive
+//     (nlm.cpp:120-142); also serves radii above the walker's instantiations.
+#pragma once
+
+#include <cstdint>
+
+#include "plgpu_walk.cuh"
+
+namespace plgpu {
+
+struct KernelBandDesc {
+  const double* src;
+  double* band;
+  int64_t n_lines, ld;
+  int32_t n, S, S_band, K;
+};
+
+// One thread per (line, diagonal d).  e[q] = extended sample at q - K.
+__global__ void banded_kernel_f64(KernelBandDesc g) {
+  const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int nd = g.S + 1;
+  if (w >= g.n_lines * nd) return;
+  const int64_t line = w / nd;
+  const int d = (int)(w % nd);
+  const int n = g.n, K = g.K;
+  const double* f = g.src + line * g.ld;
+  const int bw = 2 * g.S_band + 1;
+  double* band = g.band + line * (int64_t)n * bw;
+  auto e = [&](int q) -> double { return f[mirror_pos(q - K, n)]; };
+  double sum = 0.0;
+  for (int k = -K; k <= K; ++k) sum = __dadd_rn(sum, __dmul_rn(e(k + K), e(d + k + K)));
+  band[(int64_t)0 * bw + (d + g.S_band)] = sum;
+  band[(int64_t)d * bw + (g.S_band - d)] = sum;
+  for (int i = 1; i < n - d; ++i) {
+    const int j = i + d;
+    sum = __dsub_rn(__dadd_rn(sum, __dmul_rn(e(i + 2 * K), e(j + 2 * K))),
+                    __dmul_rn(e(i - 1), e(j - 1)));
+    band[(int64_t)i * bw + (j - i + g.S_band)] = sum;
+    band[(int64_t)j * bw + (i - j + g.S_band)] = sum;
+  }
+}
+
+struct DirectDesc {
+  const float* src;
+  float* dst;
+  int64_t n_lines, ld;
+  int32_t n, S, K;
+  float coef;
+};
+
+// One thread per pixel; clipped window ascending, direct distances.
+__global__ void __launch_bounds__(128) nlm_direct_kernel(DirectDesc g) {
+  const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= g.n_lines * g.n) return;
+  const int64_t line = w / g.n;
+  const int i = (int)(w % g.n);
+  const float* f = g.src + line * g.ld;
+  const int n = g.n, K = g.K;
+  const int lo = max(0, i - g.S), hi = min(n - 1, i + g.S);
+  float num = 0.f, den = 0.f;
+  for (int j = lo; j <= hi; ++j) {
+    float dsq = 0.f;
+    for (int t = -K; t <= K; ++t) {
+      const float df = __ldg(f + mirror_pos(i + t, n)) - __ldg(f + mirror_pos(j + t, n));
+      dsq = fmaf(df, df, dsq);
+    }
+    const float wt = ex2_approx(g.coef * dsq);
+    num = fmaf(wt, __ldg(f + j), num);
+    den += wt;
+  }
+  g.dst[line * g.ld + i] = num / den;
+}
+
+// (a + b) / 2 elementwise: average(), nlm.cpp:106-112.
+__global__ void average_kernel(const float* __restrict__ a, const float* __restrict__ b,
+                               float* __restrict__ out, int64_t count) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < count;
+       k += (int64_t)gridDim.x * blockDim.x)
+    out[k] = (a[k] + b[k]) / 2.0f;
+}
+
+}  // namespace plgpu
+
+namespace plgpu {
+
+struct Naive2DDesc {
+  const float* src;
+  float* dst;
+  int32_t batch, rows, cols, S, K;
+  float coef;
+};
+
+// Classical 2D NLM (nlm_2d_naive, nlm.cpp:168-213): one thread per pixel,
+// clipped (2S+1)^2 window, (2K+1)^2 patches over the per-axis half-sample
+// mirror (extend_symmetric_2d, nlm.cpp:84-104).  Baseline only.
+__global__ void __launch_bounds__(128) nlm_2d_naive_kernel(Naive2DDesc g) {
+  const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t plane = (int64_t)g.rows * g.cols;
+  if (w >= plane * g.batch) return;
+  const int64_t b = w / plane;
+  const int r = (int)((w % plane) / g.cols), c = (int)(w % g.cols);
+  const float* img = g.src + b * plane;
+  const int H = g.rows, W = g.cols, S = g.S, K = g.K;
+  auto px = [&](int y, int x) { return __ldg(img + (int64_t)mirror_pos(y, H) * W + mirror_pos(x, W)); };
+  float num = 0.f, den = 0.f;
+  for (int r2 = max(0, r - S); r2 <= min(H - 1, r + S); ++r2)
+    for (int c2 = max(0, c - S); c2 <= min(W - 1, c + S); ++c2) {
+      float dsq = 0.f;
+      for (int py = -K; py <= K; ++py)
+        for (int qx = -K; qx <= K; ++qx) {
+          const float df = px(r + py, c + qx) - px(r2 + py, c2 + qx);
+          dsq = fmaf(df, df, dsq);
+        }
+      const float wt = (r2 == r && c2 == c) ? 1.f : ex2_approx(g.coef * dsq);
+      num = fmaf(wt, __ldg(img + (int64_t)r2 * W + c2), num);
+      den += wt;
+    }
+  g.dst[w] = num / den;
+}
+
+}  // namespace plgpu
+
+namespace plgpu {
+
+// Direct-sum distance band for radii above the walker instantiations: one
+// thread per (line, i), (2K+1)-term sums in t-ascending order (exact on
+// integer inputs, like the walker).
+template <typename T>
+__global__ void __launch_bounds__(128) distance_band_direct_kernel(BandDesc g) {
+  const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= g.n_lines * g.n) return;
+  const int64_t line = w / g.n;
+  const int i = (int)(w % g.n);
+  const float* f = g.src + line * g.ld;
+  const int n = g.n, K = g.K, bw = 2 * g.S_band + 1;
+  T* band = reinterpret_cast<T*>(g.band) + (line * (int64_t)n + i) * bw;
+  for (int j = max(0, i - g.S); j <= min(n - 1, i + g.S); ++j) {
+    float dsq = 0.f;
+    for (int t = -K; t <= K; ++t) {
+      const float df = __ldg(f + mirror_pos(i + t, n)) - __ldg(f + mirror_pos(j + t, n));
+      dsq = fmaf(df, df, dsq);
+    }
+    band[j - i + g.S_band] = band_cast<T>(dsq);
+  }
+}
+
+}  // namespace plgpu

@@ -1,0 +1,340 @@
+"""Parity of the CUDA path (through the C ABI) against the oracle.
+
+Tolerance tiers:
+  T0  distances on integer inputs: bit-exact (int32 and fp32 exports)
+  T1  distances on float inputs:   |dd| <= 1e-5 * (1 + E_i + E_j), E = patch energy
+  T2  filter outputs:              max abs error <= 1e-3 on the [0, 255] scale
+  T3  structural invariants:       exact (transpose equivariance, constant
+                                   fixpoints, S=0 identity, batch/launch invariance)
+"""
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_1407_2343_b200 as pl  # noqa: E402
+from paper_1407_2343_b200 import workloads  # noqa: E402
+
+T2 = 1e-3
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _device():
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    pl.lib()  # fail loudly if the native library is missing
+    yield
+
+
+def dev(a, dtype=torch.float32):
+    return torch.as_tensor(np.ascontiguousarray(a), dtype=dtype).cuda()
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.cpu().numpy()
+
+
+def rand_line(rng, n, integer):
+    if integer:
+        return rng.integers(0, 256, n).astype(np.float32)
+    return rng.uniform(0, 255, n).astype(np.float32)
+
+
+# ---- T0 / T1: distances -------------------------------------------------------
+def test_integer_distances_bit_exact(orc):
+    rng = np.random.default_rng(11)
+    for _ in range(150):
+        n = int(rng.integers(1, 300))
+        K = int(rng.integers(0, min(n, 8) + 1))
+        S = int(rng.integers(0, 34))
+        f = rand_line(rng, n, True)
+        want = orc.distance_band(f, S, K)
+        got32 = host(pl.distance_band(dev(f), S, K, dtype=torch.int32))[0]
+        gotf = host(pl.distance_band(dev(f), S, K))[0]
+        mask = np.isnan(want)
+        assert np.array_equal(np.where(mask, -1, want).astype(np.int64), got32.astype(np.int64)), (n, S, K)
+        assert np.array_equal(want, gotf.astype(np.float64), equal_nan=True), (n, S, K)
+
+
+def test_c4_distances_bit_exact(orc):
+    # config 4 shape: 2048-sample integer rows of the quantised synthetic image
+    S, K, _ = workloads.params("c4")
+    img = workloads.make_config("c4", batch=1)[0]
+    rows = img[::64]  # 32 rows across the image
+    got = host(pl.distance_band(dev(rows), S, K, dtype=torch.int32))
+    for r in range(rows.shape[0]):
+        want = orc.distance_band(rows[r].astype(np.float64), S, K)
+        want = np.where(np.isnan(want), -1, want).astype(np.int64)
+        assert np.array_equal(want, got[r].astype(np.int64)), r
+
+
+def test_float_distances_t1(orc):
+    rng = np.random.default_rng(12)
+    for _ in range(60):
+        n = int(rng.integers(8, 600))
+        K = int(rng.integers(0, 9))
+        S = int(rng.integers(1, 26))
+        f = rand_line(rng, n, False).astype(np.float64)
+        want = orc.distance_band(f, S, K)
+        got = host(pl.distance_band(dev(f), S, K))[0].astype(np.float64)
+        kern, _ = orc.banded_kernel(f, S, K)
+        energy = kern[:, S]
+        i = np.arange(n)[:, None]
+        j = i + np.arange(-S, S + 1)[None, :]
+        ok = ~np.isnan(want)
+        tol = 1e-5 * (1 + energy[i.repeat(2 * S + 1, 1)] + energy[np.clip(j, 0, n - 1)])
+        assert np.array_equal(np.isnan(got), ~ok)
+        assert np.all(np.abs(got - want)[ok] <= tol[ok]), (n, S, K)
+
+
+def test_banded_kernel_f64_bit_equal(orc):
+    rng = np.random.default_rng(13)
+    for _ in range(60):
+        n = int(rng.integers(1, 120))
+        K = int(rng.integers(0, min(n, 8) + 1))
+        S = int(rng.integers(0, 20))
+        f = rng.uniform(0, 255, n)
+        want, _ = orc.banded_kernel(f, S, K)
+        got = host(pl.banded_kernel_f64(dev(f, torch.float64), S, K))[0]
+        assert np.array_equal(want, got, equal_nan=True), (n, S, K)
+
+
+# ---- T2: filter outputs ----------------------------------------------------------
+def test_lines_vs_oracle(orc):
+    rng = np.random.default_rng(21)
+    worst = 0.0
+    for t in range(200):
+        n = int(rng.integers(1, 400))
+        S = int(rng.integers(0, 40))
+        K = int(rng.integers(0, min(n, 9) + 1))
+        h = float(np.exp(rng.uniform(np.log(15.0), np.log(1000.0))))
+        f = rand_line(rng, n, t % 3 == 0)
+        want = orc.nlm_1d(f.astype(np.float64), S, K, h)
+        got = host(pl.nlm_1d_patchlift(dev(f), (S, K, h))).astype(np.float64)
+        worst = max(worst, float(np.abs(got - want).max()))
+        assert np.abs(got - want).max() <= T2, (n, S, K, h)
+    print("worst T2 error over random lines:", worst)
+
+
+def test_naive_route_vs_oracle(orc):
+    rng = np.random.default_rng(22)
+    for _ in range(40):
+        n = int(rng.integers(1, 200))
+        S = int(rng.integers(0, 20))
+        K = int(rng.integers(0, min(n, 6) + 1))
+        h = float(np.exp(rng.uniform(np.log(15.0), np.log(1000.0))))
+        f = rand_line(rng, n, False)
+        want = orc.nlm_1d(f.astype(np.float64), S, K, h, naive=True)
+        got = host(pl.nlm_1d_naive(dev(f), (S, K, h))).astype(np.float64)
+        assert np.abs(got - want).max() <= T2
+
+
+def test_c1_full_vs_golden(golden):
+    S, K, h = workloads.params("c1")
+    f = workloads.make_config("c1")
+    got = host(pl.nlm_1d_patchlift(dev(f), (S, K, h)))
+    err = np.abs(got.astype(np.float64) - golden["c1_nlm"].astype(np.float64)).max()
+    assert err <= T2, err
+
+
+def test_images_vs_oracle(orc):
+    rng = np.random.default_rng(26)
+    shapes = [(1, 1), (1, 7), (7, 1), (2, 3), (14, 9), (24, 17), (33, 40), (64, 64), (130, 257),
+              (300, 129)]
+    for r, c in shapes:
+        for S, K in [(0, 0), (1, 0), (4, 2), (10, 3), (15, 5), (25, 7), (40, 1)]:
+            if K > min(r, c):
+                continue
+            h = float(np.exp(rng.uniform(np.log(15.0), np.log(1000.0))))
+            img = rng.uniform(0, 255, (r, c)).astype(np.float32)
+            x = dev(img)
+            for op, fn in (("row", pl.nlm_row_pass), ("col", pl.nlm_col_pass),
+                           ("rc", pl.snlm_2d_row_col), ("cr", pl.snlm_2d_col_row),
+                           ("snlm", pl.snlm_2d)):
+                want = orc.filter(op, img.astype(np.float64), S, K, h, threads=4)
+                got = host(fn(x, (S, K, h))).astype(np.float64)
+                assert np.abs(got - want).max() <= T2, (r, c, S, K, op)
+
+
+def test_golden_images_t2(golden):
+    for t, (r, c, S, K, h) in enumerate(golden["image_cases"]):
+        x = dev(golden[f"i{t}_img"])
+        for op, fn in (("row", pl.nlm_row_pass), ("col", pl.nlm_col_pass),
+                       ("rc", pl.snlm_2d_row_col), ("cr", pl.snlm_2d_col_row), ("snlm", pl.snlm_2d)):
+            got = host(fn(x, (int(S), int(K), h))).astype(np.float64)
+            assert np.abs(got - golden[f"i{t}_{op}"]).max() <= T2, (t, op)
+
+
+def test_c2_rc_vs_oracle(orc):
+    S, K, h = workloads.params("c2")
+    img = workloads.make_config("c2")[0]
+    want = orc.snlm_rc(img.astype(np.float64), S, K, h, threads=8)
+    got = host(pl.snlm_2d_row_col(dev(img), (S, K, h))).astype(np.float64)
+    assert np.abs(got - want).max() <= T2
+
+
+@pytest.mark.slow
+def test_c3_rc_vs_oracle(orc):
+    S, K, h = workloads.params("c3")
+    img = workloads.make_config("c3")[0]
+    got = host(pl.snlm_2d_row_col(dev(img), (S, K, h))).astype(np.float64)
+    rows = slice(0, 4096, 97)  # a sampled stripe keeps the CPU check to seconds
+    want_rows = orc.row_pass(img.astype(np.float64), S, K, h, threads=8)
+    want = orc.col_pass(want_rows, S, K, h, threads=8)
+    assert np.abs(got[rows] - want[rows]).max() <= T2
+
+
+def test_c4_batch_rc_vs_oracle(orc):
+    S, K, h = workloads.params("c4")
+    imgs = workloads.make_config("c4", batch=2)
+    got = host(pl.snlm_2d_row_col(dev(imgs), (S, K, h))).astype(np.float64)
+    for b in range(2):
+        want = orc.snlm_rc(imgs[b].astype(np.float64), S, K, h, threads=8)
+        assert np.abs(got[b] - want).max() <= T2
+
+
+# ---- T3: structural invariants ----------------------------------------------------
+def test_transpose_equivariance_bitwise():
+    rng = np.random.default_rng(3001)
+    for r, c, S, K, h in [(24, 17, 5, 2, 40.0), (12, 15, 5, 1, 45.0), (200, 333, 15, 5, 140.0),
+                          (64, 300, 10, 3, 74.8)]:
+        img = rng.uniform(0, 255, (r, c)).astype(np.float32)
+        x, xt = dev(img), dev(img.T)
+        p = (S, K, h)
+        assert np.array_equal(host(pl.snlm_2d(xt, p)), host(pl.snlm_2d(x, p)).T)
+        assert np.array_equal(host(pl.snlm_2d_row_col(xt, p)), host(pl.snlm_2d_col_row(x, p)).T)
+        assert np.array_equal(host(pl.snlm_2d_col_row(xt, p)), host(pl.snlm_2d_row_col(x, p)).T)
+        assert np.array_equal(host(pl.nlm_col_pass(x, p)), host(pl.nlm_row_pass(xt, p)).T)
+
+
+def test_snlm_is_mean_of_orders_bitwise():
+    img = np.random.default_rng(27).uniform(0, 255, (40, 52)).astype(np.float32)
+    x = dev(img)
+    p = (5, 1, 45.0)
+    rc = host(pl.snlm_2d_row_col(x, p))
+    cr = host(pl.snlm_2d_col_row(x, p))
+    assert np.array_equal(host(pl.snlm_2d(x, p)), (rc + cr) / np.float32(2))
+
+
+def test_constant_fixpoints_exact():
+    for c in (0.0, 0.5, 100.0, 255.0):
+        f = np.full(40, c, np.float32)
+        assert np.array_equal(host(pl.nlm_1d_patchlift(dev(f), (5, 2, 30.0))), f)
+        img = np.full((12, 17), c, np.float32)
+        for fn in (pl.snlm_2d, pl.snlm_2d_row_col, pl.nlm_row_pass, pl.nlm_col_pass, pl.nlm_2d_naive):
+            assert np.array_equal(host(fn(dev(img), (6, 2, 30.0))), img)
+        big = np.full((3, 300, 260), c, np.float32)
+        assert np.array_equal(host(pl.snlm_2d_row_col(dev(big), (15, 5, 30.0))), big)
+
+
+def test_s0_identity_exact():
+    rng = np.random.default_rng(22)
+    f = rng.uniform(0, 255, 33).astype(np.float32)
+    assert np.array_equal(host(pl.nlm_1d_patchlift(dev(f), (0, 3, 25.0))), f)
+    img = rng.uniform(0, 255, (9, 13)).astype(np.float32)
+    for fn in (pl.snlm_2d, pl.snlm_2d_row_col, pl.snlm_2d_col_row):
+        assert np.array_equal(host(fn(dev(img), (0, 3, 25.0))), img)
+
+
+def test_h_infinity_window_mean():
+    # nlm_test.cpp:114-141 re-tiered: fp32 window mean, tolerance 1e-4
+    f = np.random.default_rng(23).uniform(0, 255, 64).astype(np.float32)
+    S = 7
+    got = host(pl.nlm_1d_patchlift(dev(f), (S, 2, 1e9)))
+    for i in range(64):
+        lo, hi = max(0, i - S), min(63, i + S)
+        assert abs(got[i] - f[lo:hi + 1].astype(np.float64).mean()) <= 1e-4
+
+
+def test_convex_bounds():
+    # acceptance_main.cpp:258-283 on the device: output inside [min, max] of input
+    rng = np.random.default_rng(105)
+    for t in range(40):
+        img = rng.uniform(0, 255, (64, 64)).astype(np.float32)
+        p = (1 + int(rng.integers(0, 8)), int(rng.integers(0, 5)),
+             float(np.exp(rng.uniform(np.log(0.5), np.log(5000.0)))))
+        for fn in (pl.snlm_2d, pl.nlm_2d_naive):
+            out = host(fn(dev(img), p))
+            assert out.min() >= img.min() and out.max() <= img.max(), (t, p)
+
+
+def test_batch_and_launch_invariance_bitwise():
+    rng = np.random.default_rng(28)
+    imgs = rng.uniform(0, 255, (5, 150, 190)).astype(np.float32)
+    p = (10, 3, 74.8)
+    whole = host(pl.snlm_2d_row_col(dev(imgs), p))
+    for b in range(5):
+        assert np.array_equal(host(pl.snlm_2d_row_col(dev(imgs[b]), p)), whole[b])
+    again = host(pl.snlm_2d_row_col(dev(imgs), p))
+    assert np.array_equal(whole, again)  # deterministic
+
+
+def test_lines_batch_invariance_bitwise():
+    rng = np.random.default_rng(30)
+    x = rng.uniform(0, 255, (37, 1000)).astype(np.float32)
+    p = (15, 5, 140.0)
+    allr = host(pl.nlm_1d_patchlift(dev(x), p))
+    for r in (0, 5, 36):
+        assert np.array_equal(host(pl.nlm_1d_patchlift(dev(x[r]), p)), allr[r])
+
+
+def test_blocked_row_pass_layout():
+    rng = np.random.default_rng(31)
+    img = rng.uniform(0, 255, (96, 256)).astype(np.float32)
+    p = (10, 3, 74.8)
+    plain = host(pl.nlm_row_pass(dev(img), p))
+    for cb in (32, 64, 128, 256):
+        blk = host(pl.nlm_row_pass_blocked(dev(img), p, cb))
+        want = plain.reshape(96, 256 // cb, cb).transpose(1, 0, 2).reshape(-1)
+        assert np.array_equal(blk.reshape(-1), want), cb
+
+
+def test_host_e2e_matches_device():
+    rng = np.random.default_rng(32)
+    imgs = rng.uniform(0, 255, (3, 128, 200)).astype(np.float32)
+    p = (10, 3, 74.8)
+    dev_out = host(pl.snlm_2d_row_col(dev(imgs), p))
+    host_out = pl.snlm_2d_row_col_host(imgs, p)
+    assert np.array_equal(dev_out, host_out)
+
+
+def test_validation_errors_raise():
+    x = dev(np.ones((5, 9), np.float32))
+    with pytest.raises(pl.ValidationError, match="patch radius exceeds signal length"):
+        pl.snlm_2d(x, (2, 6, 5.0))
+    with pytest.raises(pl.ValidationError, match="smoothing parameter h must be positive"):
+        pl.snlm_2d(x, (2, 1, -1.0))
+    with pytest.raises(pl.ValidationError, match="search radius must be nonnegative"):
+        pl.nlm_1d_patchlift(dev(np.ones(5, np.float32)), (-1, 1, 5.0))
+
+
+def test_nlm_2d_naive_vs_reference(ref):
+    rng = np.random.default_rng(33)
+    img = rng.uniform(0, 255, (23, 17)).astype(np.float32)
+    for p in [(4, 1, 35.0), (3, 2, 60.0)]:
+        want = ref.filter("nlm2d", img.astype(np.float64), *p)
+        got = host(pl.nlm_2d_naive(dev(img), p)).astype(np.float64)
+        assert np.abs(got - want).max() <= T2
+
+
+def test_rc_vs_reference_library(ref):
+    """The CUDA path against the reference's own snlm_2d_row_col (oracle/_ref)."""
+    S, K, h = workloads.params("c2")
+    img = workloads.make_config("c2")[0][:256, :320]
+    want = ref.filter("rc", img.astype(np.float64), S, K, h, threads=0)
+    got = host(pl.snlm_2d_row_col(dev(img), (S, K, h))).astype(np.float64)
+    assert np.abs(got - want).max() <= T2
+
+
+def test_cpp_dropin_library():
+    """libpatchlift_b200 through the reference's C++ API (tests/cpp/dropin_check.cpp)."""
+    import os
+    import subprocess
+    exe = os.path.join(pl.LIBDIR, "dropin_check")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    print(r.stdout[-4000:])
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
