@@ -108,7 +108,7 @@ __global__ void direct_pass_kernel(plgpu::PassDesc g) {
   const int64_t ps = g.src_pos_stride;
   const int n = g.n, K = g.K;
   const int lo = max(0, i - g.S), hi = min(n - 1, i + g.S);
-  float num = 0.f, den = 0.f;
+  float num = 0.f, den = 0.f, vmin = 3.402823466e38f, vmax = -3.402823466e38f;
   for (int j = lo; j <= hi; ++j) {
     float dsq = 0.f;
     for (int t = -K; t <= K; ++t) {
@@ -117,13 +117,16 @@ __global__ void direct_pass_kernel(plgpu::PassDesc g) {
       dsq = fmaf(df, df, dsq);
     }
     const float wt = (j == i) ? 1.f : plgpu::ex2_approx(g.coef * dsq);
-    num = fmaf(wt, __ldg(f + (int64_t)j * ps), num);
+    const float fj = __ldg(f + (int64_t)j * ps);
+    num = fmaf(wt, fj, num);
     den += wt;
+    vmin = fminf(vmin, fj);
+    vmax = fmaxf(vmax, fj);
   }
   const int blk = g.dst_pos_block;
   float* dst = g.dst + img * g.dst_img_stride + li * g.dst_line_stride +
                (int64_t)(i / blk) * g.dst_block_stride + (int64_t)(i % blk) * g.dst_pos_stride;
-  *dst = num / den;
+  *dst = fminf(fmaxf(num / den, vmin), vmax);
 }
 
 int run_pass(plgpu::PassDesc g, const pl_params& p, cudaStream_t st) {

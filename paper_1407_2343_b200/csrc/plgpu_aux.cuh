@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(128) nlm_direct_kernel(DirectDesc g) {
   const float* f = g.src + line * g.ld;
   const int n = g.n, K = g.K;
   const int lo = max(0, i - g.S), hi = min(n - 1, i + g.S);
-  float num = 0.f, den = 0.f;
+  float num = 0.f, den = 0.f, vmin = 3.402823466e38f, vmax = -3.402823466e38f;
   for (int j = lo; j <= hi; ++j) {
     float dsq = 0.f;
     for (int t = -K; t <= K; ++t) {
@@ -70,10 +70,13 @@ __global__ void __launch_bounds__(128) nlm_direct_kernel(DirectDesc g) {
       dsq = fmaf(df, df, dsq);
     }
     const float wt = ex2_approx(g.coef * dsq);
-    num = fmaf(wt, __ldg(f + j), num);
+    const float fj = __ldg(f + j);
+    num = fmaf(wt, fj, num);
     den += wt;
+    vmin = fminf(vmin, fj);
+    vmax = fmaxf(vmax, fj);
   }
-  g.dst[line * g.ld + i] = num / den;
+  g.dst[line * g.ld + i] = fminf(fmaxf(num / den, vmin), vmax);
 }
 
 // (a + b) / 2 elementwise: average(), nlm.cpp:106-112.
@@ -107,7 +110,7 @@ __global__ void __launch_bounds__(128) nlm_2d_naive_kernel(Naive2DDesc g) {
   const float* img = g.src + b * plane;
   const int H = g.rows, W = g.cols, S = g.S, K = g.K;
   auto px = [&](int y, int x) { return __ldg(img + (int64_t)mirror_pos(y, H) * W + mirror_pos(x, W)); };
-  float num = 0.f, den = 0.f;
+  float num = 0.f, den = 0.f, vmin = 3.402823466e38f, vmax = -3.402823466e38f;
   for (int r2 = max(0, r - S); r2 <= min(H - 1, r + S); ++r2)
     for (int c2 = max(0, c - S); c2 <= min(W - 1, c + S); ++c2) {
       float dsq = 0.f;
@@ -117,10 +120,13 @@ __global__ void __launch_bounds__(128) nlm_2d_naive_kernel(Naive2DDesc g) {
           dsq = fmaf(df, df, dsq);
         }
       const float wt = (r2 == r && c2 == c) ? 1.f : ex2_approx(g.coef * dsq);
-      num = fmaf(wt, __ldg(img + (int64_t)r2 * W + c2), num);
+      const float v = __ldg(img + (int64_t)r2 * W + c2);
+      num = fmaf(wt, v, num);
       den += wt;
+      vmin = fminf(vmin, v);
+      vmax = fmaxf(vmax, v);
     }
-  g.dst[w] = num / den;
+  g.dst[w] = fminf(fmaxf(num / den, vmin), vmax);
 }
 
 }  // namespace plgpu

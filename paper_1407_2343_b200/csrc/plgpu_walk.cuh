@@ -95,10 +95,16 @@ __device__ __forceinline__ void walk_segment(const PassDesc& g, const float* __r
   float fr[R], nr[R], orr[R];  // rings: f[i+q], e[i+K+q], e[i-1-K+q]
   float d[R];                  // d[k], k = 1..ST (d[0] unused)
   float an[R], ad[R];          // pending num/den of pixel i+q
+  // Range of every sample the segment's windows can touch: outputs are
+  // clamped into it, so fp32 rounding of num/den can never leave the input
+  // range (the convex-combination guarantee, acceptance_main.cpp:256-283).
+  float lo = 3.402823466e38f, hi = -3.402823466e38f;
 
 #pragma unroll
   for (int q = 0; q < R; ++q) {
     fr[q] = ld(i0 + q);
+    lo = fminf(lo, fr[q]);
+    hi = fmaxf(hi, fr[q]);
     nr[q] = ld(i0 + K + q);
     orr[q] = ld(i0 - 1 - K + q);
     an[q] = 0.f;
@@ -126,10 +132,11 @@ __device__ __forceinline__ void walk_segment(const PassDesc& g, const float* __r
       const int s = sb + r;
       if (s >= T) break;
       const int i = i0 + s;
-      // Entering samples for step s+1 (prefetched one step ahead).
-      const float tf = ld(i + 1 + S);
-      const float tn = ld(i + 1 + K + S);
-      const float to = ld(i - K + S);
+      // Entering samples for step s+1 (prefetched one step ahead): the ring
+      // slot r advances by R = ST+1 positions.
+      const float tf = ld(i + 1 + ST);
+      const float tn = ld(i + 1 + K + ST);
+      const float to = ld(i - K + ST);
       const float an_ = nr[r], ao = orr[r], fi = fr[r];
       const int kmax = EDGE ? min(S, n - 1 - i) : ST;
       float num = an[r] + fi;  // j-side contributions so far + centre (w = 1)
@@ -150,7 +157,8 @@ __device__ __forceinline__ void walk_segment(const PassDesc& g, const float* __r
         ad[rk] += w;
       }
       if (i >= s0) {
-        *op = num / den;  // IEEE div.rn: constant lines stay exact fixpoints
+        // IEEE div.rn: constant lines stay exact fixpoints
+        *op = fminf(fmaxf(num / den, lo), hi);
         op += dps;
         if (--orem == 0) {
           op += g.dst_block_stride - (int64_t)blk * dps;
@@ -159,6 +167,8 @@ __device__ __forceinline__ void walk_segment(const PassDesc& g, const float* __r
       }
       an[r] = 0.f;
       ad[r] = 0.f;
+      lo = fminf(lo, tf);
+      hi = fmaxf(hi, tf);
       fr[r] = tf;
       nr[r] = tn;
       orr[r] = to;
@@ -243,8 +253,8 @@ __global__ void __launch_bounds__(128) distance_band_kernel(BandDesc g) {
       const int s = sb + r;
       if (s >= s1 - i0) break;
       const int i = i0 + s;
-      const float tn = ld(i + 1 + K + S);
-      const float to = ld(i - K + S);
+      const float tn = ld(i + 1 + K + ST);
+      const float to = ld(i - K + ST);
       const float an_ = nr[r], ao = orr[r];
       if (i >= s0) band[(int64_t)i * bw + g.S_band] = band_cast<T>(0.f);
 #pragma unroll
