@@ -172,6 +172,8 @@ def mufu_peak():
     ms = C.c_double(0)
     ex2 = L.plub_rate(0, 8, 256, 4096, C.byref(ms))
     ffma = L.plub_rate(1, 8, 256, 4096, C.byref(ms))
+    ffma2 = L.plub_rate(2, 8, 256, 4096, C.byref(ms))
+    mufu_peak.ffma2 = ffma2 if ffma2 > 0 else None
     return (ex2 if ex2 > 0 else None), (ffma if ffma > 0 else None)
 
 
@@ -366,6 +368,7 @@ def run_ours(args):
         "hbm": {"achieved_gbs": hbm_bytes / (t_dom * 1e-3) / 1e9, "peak_gbs": peaks.get("hbm_gbs"),
                 "t_hbm_ms": hbm_bytes / (peaks.get("hbm_gbs", 6541.5) * 1e9) * 1e3},
         "ffma_peak_gflops_measured": (ffma_peak / 1e9) if ffma_peak else None,
+        "ffma2_peak_gflops_measured": (getattr(mufu_peak, "ffma2", None) or 0) / 1e9 or None,
     }
 
     line = None

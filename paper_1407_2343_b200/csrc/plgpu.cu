@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -63,10 +64,34 @@ int validate_image(int batch, int rows, int cols) {
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 // Segment length: a function of the line length (and S) only.
+// Segment length: a function of (n, S) only, identical for rows and columns
+// (transpose equivariance) and for every launch shape.  About 256 samples,
+// trimmed so that an interior segment's walk (C + S steps, S of pre-walk) is a
+// whole number of S+1-step iterations of the unrolled walker.
 int32_t segment_length(int32_t n, int32_t S) {
-  (void)S;
-  const int32_t C = 128;
+  const int32_t R = std::max(1, S + 1);
+  const int32_t C = 256 - (256 + S) % R;
   return n < C ? n : C;
+}
+
+// Kernel selection: the production walker (plgpu_walk2.cuh) serves K <= 7 on
+// either axis; the portable walker (plgpu_walk.cuh, same arithmetic, bitwise
+// equal results) serves larger patch radii.  PLGPU_FORCE_WALKER=1 forces the
+// portable one (used by the tests to prove the two agree bit for bit).
+bool force_portable() {
+  static const bool f = [] {
+    const char* e = std::getenv("PLGPU_FORCE_WALKER");
+    return e && e[0] == '1';
+  }();
+  return f;
+}
+// PLGPU_FORCE_WALKER=2 skips only the hot-configuration kernel (walk3).
+bool force_portable_v2() {
+  static const bool f = [] {
+    const char* e = std::getenv("PLGPU_FORCE_WALKER");
+    return e && e[0] == '2';
+  }();
+  return f;
 }
 
 // Largest radius with a specialised walker; larger radii use the direct kernel.
@@ -129,6 +154,90 @@ __global__ void direct_pass_kernel(plgpu::PassDesc g) {
   *dst = fminf(fmaxf(num / den, vmin), vmax);
 }
 
+// Production walker launch, if the geometry qualifies (returns -1 if not).
+int try_pass2(const plgpu::PassDesc& g, cudaStream_t st) {
+  // A warp carries 32-64 lines: for a handful of lines the one-thread-per-
+  // segment portable walker wastes less.
+  if (force_portable() || g.K > 7 || g.S < 1 || g.S > kMaxWalkS || g.lines_per_img < 16) return -1;
+  const int ST = template_radius(g.S);
+  const int LW = 32 * plgpu::pass2_lines(ST);
+  const bool rows = g.src_pos_stride == 1 && g.dst_pos_stride == 1;
+  const bool cols = g.src_line_stride == 1 && g.dst_line_stride == 1;
+  if (!rows && !cols) return -1;
+  if (rows && g.dst_pos_block != g.n && g.dst_pos_block % plgpu::kCH != 0) return -1;
+  if (!rows && g.dst_pos_block != g.n) return -1;
+  plgpu::Pass2Desc d{};
+  d.src = g.src;
+  d.dst = g.dst;
+  d.src_img_stride = g.src_img_stride;
+  d.src_line_stride = g.src_line_stride;
+  d.src_pos_stride = g.src_pos_stride;
+  d.dst_img_stride = g.dst_img_stride;
+  d.dst_line_stride = g.dst_line_stride;
+  d.dst_pos_stride = g.dst_pos_stride;
+  d.dst_block_stride = g.dst_block_stride;
+  d.dst_pos_block = g.dst_pos_block;
+  d.lines_per_img = g.lines_per_img;
+  d.groups_per_img = (g.lines_per_img + LW - 1) / LW;
+  d.n = g.n;
+  d.seg_len = g.seg_len;
+  d.nseg = g.nseg;
+  d.S = g.S;
+  d.K = g.K;
+  d.coef = g.coef;
+  const int64_t images = g.n_lines / g.lines_per_img;
+  d.total_warps = images * d.groups_per_img * d.nseg;
+  const auto a16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  d.vec16 = !rows && g.lines_per_img % LW == 0 && g.src_pos_stride % 4 == 0 &&
+            g.src_img_stride % 4 == 0 && g.dst_pos_stride % 2 == 0 && g.dst_img_stride % 2 == 0 &&
+            a16(g.src) && a16(g.dst);
+  if (!force_portable_v2()) {
+    // hot (K, S) pairs: compile-time-K kernel with interior/edge warp ordering
+    const int KT3 = plgpu::pass3_k_for(ST);
+    if (KT3 == g.K && ST == g.S) {
+      const int R = ST + 1, BASE = ST + 2 * KT3 + 2;
+      plgpu::Pass3Desc d3{};
+      d3.b = d;
+      int lo = d.nseg, hi = -1;
+      for (int sgi = 0; sgi < d.nseg; ++sgi) {
+        const int s0 = sgi * d.seg_len, s1 = std::min(d.n, s0 + d.seg_len);
+        const int i0 = std::max(0, s0 - d.S), T = s1 - i0, pos0 = i0 - 1 - d.K;
+        const int nch = (T + R - 1) / R;
+        const bool interior = pos0 >= 0 && pos0 + nch * R + BASE - 1 <= d.n - 1 && T % R == 0;
+        if (interior) {
+          lo = std::min(lo, sgi);
+          hi = std::max(hi, sgi);
+        }
+      }
+      if (hi < lo) {
+        lo = 0;
+        hi = -1;
+      }
+      d3.seg_lo = lo;
+      d3.seg_hi = hi;
+      const int64_t groups = d.total_warps / d.nseg;
+      d3.interior_warps = groups * std::max(0, hi - lo + 1);
+      bool launched = false;
+      switch (ST) {
+#define PL_CASE(v) \
+  case v: launched = plgpu::launch_pass3<v>(d3, rows, st); break;
+        PLGPU_FOR_EACH_RADIUS(PL_CASE)
+#undef PL_CASE
+      }
+      if (launched) return check_launch();
+    }
+  }
+  switch (ST) {
+#define PL_CASE(v) \
+  case v: plgpu::launch_pass2<v>(d, rows, st); break;
+    PLGPU_FOR_EACH_RADIUS(PL_CASE)
+#undef PL_CASE
+    default:
+      return -1;
+  }
+  return check_launch();
+}
+
 int run_pass(plgpu::PassDesc g, const pl_params& p, cudaStream_t st) {
   g.S = std::min<int32_t>(p.search_radius, g.n - 1);
   g.K = p.patch_radius;
@@ -137,6 +246,10 @@ int run_pass(plgpu::PassDesc g, const pl_params& p, cudaStream_t st) {
   g.nseg = (g.n + g.seg_len - 1) / g.seg_len;
   if (g.dst_pos_block <= 0) g.dst_pos_block = g.n;
   if (g.n_lines <= 0) return PL_OK;
+  if (g.n_lines % g.lines_per_img == 0) {
+    const int rc = try_pass2(g, st);
+    if (rc >= 0) return rc;
+  }
   if (g.S >= 1 && g.S <= kMaxWalkS) return dispatch_pass(g, st);
   const int64_t work = g.n_lines * g.n;
   direct_pass_kernel<<<(unsigned)((work + 127) / 128), 128, 0, st>>>(g);

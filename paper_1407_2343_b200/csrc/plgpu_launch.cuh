@@ -7,6 +7,8 @@
 #include <cuda_runtime.h>
 
 #include "plgpu_walk.cuh"
+#include "plgpu_walk2.cuh"
+#include "plgpu_walk3.cuh"
 
 namespace plgpu {
 
@@ -15,6 +17,18 @@ void launch_pass(const PassDesc& g, cudaStream_t st);
 
 template <int ST, typename T>
 void launch_band(const BandDesc& g, cudaStream_t st);
+
+// Production pass kernel (plgpu_walk2.cuh): LINES = 2 (packed f32x2) for
+// radii <= 16, 1 above (register budget); rows selects the transposing stage.
+template <int ST>
+void launch_pass2(const Pass2Desc& g, bool rows, cudaStream_t st);
+constexpr int pass2_lines(int ST) { return ST <= 16 ? 2 : 1; }
+
+// Hot-configuration kernel (plgpu_walk3.cuh) for the (K, S) pairs of the
+// configs; returns false if (g.K, ST) has no instantiation.
+template <int ST>
+bool launch_pass3(const Pass3Desc& d, bool rows, cudaStream_t st);
+constexpr int pass3_k_for(int ST) { return ST == 10 ? 3 : ST == 15 ? 5 : ST == 25 ? 7 : -1; }
 
 #ifdef PLGPU_DEFINE_LAUNCHERS
 template <int ST>
@@ -31,8 +45,56 @@ void launch_band(const BandDesc& g, cudaStream_t st) {
   distance_band_kernel<ST, T><<<(unsigned)((work + 127) / 128), 128, 0, st>>>(g);
 }
 
+// Compile-time patch radius served by the single-ring form for this search
+// radius (the configs' (K, S) pairs), or -1.
+constexpr int fixed_k_for(int ST) { return ST < 0 ? ST : -1; }  // single-ring form disabled: spills
+
+template <int ST, int KT>
+void launch_pass2_k(const Pass2Desc& g, bool rows, cudaStream_t st) {
+  constexpr int L = pass2_lines(ST);
+  const unsigned blocks = (unsigned)((g.total_warps + kWarpsPerCta - 1) / kWarpsPerCta);
+  if (rows) {
+    const size_t smem = sizeof(float) * kWarpsPerCta * pass2_smem_floats_per_warp<L, true>();
+    nlm_pass2_kernel<ST, KT, L, true><<<blocks, 32 * kWarpsPerCta, smem, st>>>(g);
+  } else {
+    const size_t smem = sizeof(float) * kWarpsPerCta * pass2_smem_floats_per_warp<L, false>();
+    nlm_pass2_kernel<ST, KT, L, false><<<blocks, 32 * kWarpsPerCta, smem, st>>>(g);
+  }
+}
+
+template <int ST>
+void launch_pass2(const Pass2Desc& g, bool rows, cudaStream_t st) {
+  constexpr int KF = fixed_k_for(ST);
+  if constexpr (KF >= 0) {
+    if (g.K == KF && g.S == ST) return launch_pass2_k<ST, KF>(g, rows, st);
+  }
+  launch_pass2_k<ST, -1>(g, rows, st);
+}
+
+template <int ST>
+bool launch_pass3(const Pass3Desc& d, bool rows, cudaStream_t st) {
+  constexpr int KT = pass3_k_for(ST);
+  if constexpr (KT < 0) {
+    return false;
+  } else {
+    if (d.b.K != KT || d.b.S != ST) return false;
+    constexpr int L = pass2_lines(ST);
+    const unsigned blocks = (unsigned)((d.b.total_warps + kWarpsPerCta - 1) / kWarpsPerCta);
+    if (rows) {
+      const size_t smem = sizeof(float) * kWarpsPerCta * pass3_smem_floats_per_warp<ST, L, true>();
+      nlm_pass3_kernel<ST, KT, L, true><<<blocks, 32 * kWarpsPerCta, smem, st>>>(d);
+    } else {
+      const size_t smem = sizeof(float) * kWarpsPerCta * pass3_smem_floats_per_warp<ST, L, false>();
+      nlm_pass3_kernel<ST, KT, L, false><<<blocks, 32 * kWarpsPerCta, smem, st>>>(d);
+    }
+    return true;
+  }
+}
+
 #define PLGPU_INSTANTIATE(ST)                                              \
+  template bool launch_pass3<ST>(const Pass3Desc&, bool, cudaStream_t);    \
   template void launch_pass<ST>(const PassDesc&, cudaStream_t);            \
+  template void launch_pass2<ST>(const Pass2Desc&, bool, cudaStream_t);    \
   template void launch_band<ST, float>(const BandDesc&, cudaStream_t);     \
   template void launch_band<ST, int32_t>(const BandDesc&, cudaStream_t);
 #endif

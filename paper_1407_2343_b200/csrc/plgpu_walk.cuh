@@ -65,6 +65,18 @@ __device__ __forceinline__ float ex2_approx(float x) {
   return y;
 }
 
+// num / den for the filter output: one MUFU.RCP plus one correction step
+// q' = q + r (num - den q) (Markstein).  When the true quotient is
+// representable (e.g. constant inputs: num = m c, den = m) it is returned
+// exactly; otherwise the result is within one ulp of the IEEE quotient.
+// Both walkers use it, so their outputs stay bitwise equal.
+__device__ __forceinline__ float div_fix(float num, float den) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(den));
+  const float q = num * r;
+  return fmaf(fmaf(-den, q, num), r, q);
+}
+
 // Half-sample mirror (core_types.cpp:71-88) extended by a clamp: positions
 // beyond the extension only ever feed pairs that are masked out.
 __device__ __forceinline__ int mirror_pos(int p, int n) {
@@ -157,8 +169,7 @@ __device__ __forceinline__ void walk_segment(const PassDesc& g, const float* __r
         ad[rk] += w;
       }
       if (i >= s0) {
-        // IEEE div.rn: constant lines stay exact fixpoints
-        *op = fminf(fmaxf(num / den, lo), hi);
+        *op = fminf(fmaxf(div_fix(num, den), lo), hi);
         op += dps;
         if (--orem == 0) {
           op += g.dst_block_stride - (int64_t)blk * dps;

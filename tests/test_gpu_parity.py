@@ -344,3 +344,35 @@ def test_cpp_dropin_library():
     r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     print(r.stdout[-4000:])
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
+
+
+def test_portable_and_production_walkers_bitwise_equal(tmp_path):
+    """The production walker (smem-staged, packed f32x2) and the portable one
+    (plgpu_walk.cuh) run the same per-line arithmetic: outputs are bitwise equal."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import sys, numpy as np, torch; sys.path.insert(0, %r)\n"
+        "import paper_1407_2343_b200 as pl\n"
+        "rng = np.random.default_rng(5)\n"
+        "outs = {}\n"
+        "for (b, r, c, S, K) in [(2, 300, 517, 10, 3), (1, 260, 700, 15, 5), (1, 333, 290, 25, 7),"
+        " (3, 64, 128, 4, 2), (1, 40, 1000, 32, 7), (2, 1100, 96, 10, 3), (1, 70, 1500, 15, 5),"
+        " (1, 900, 100, 25, 7), (1, 7, 3000, 10, 3)]:\n"
+        "    x = torch.from_numpy(rng.uniform(0, 255, (b, r, c)).astype(np.float32)).cuda()\n"
+        "    p = (S, K, 50.0 + 10 * S)\n"
+        "    outs[f'{r}x{c}_rc'] = pl.snlm_2d_row_col(x, p).cpu().numpy()\n"
+        "    outs[f'{r}x{c}_cr'] = pl.snlm_2d_col_row(x, p).cpu().numpy()\n"
+        "np.savez(sys.argv[1], **outs)\n" % os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    files = []
+    for force in ("0", "1", "2"):  # production(walk3/walk2), portable, walk2 only
+        f = str(tmp_path / f"out{force}.npz")
+        env = dict(os.environ, PLGPU_FORCE_WALKER=force)
+        r = subprocess.run([sys.executable, "-c", code, f], env=env, capture_output=True, text=True,
+                           timeout=600)
+        assert r.returncode == 0, r.stderr[-3000:]
+        files.append(np.load(f))
+    for key in files[0].files:
+        assert np.array_equal(files[0][key], files[1][key]), key
+        assert np.array_equal(files[0][key], files[2][key]), key
