@@ -189,7 +189,7 @@ int try_pass2(const plgpu::PassDesc& g, cudaStream_t st) {
   d.total_warps = images * d.groups_per_img * d.nseg;
   const auto a16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   d.vec16 = !rows && g.lines_per_img % LW == 0 && g.src_pos_stride % 4 == 0 &&
-            g.src_img_stride % 4 == 0 && g.dst_pos_stride % 2 == 0 && g.dst_img_stride % 2 == 0 &&
+            g.src_img_stride % 4 == 0 && g.dst_pos_stride % 4 == 0 && g.dst_img_stride % 4 == 0 &&
             a16(g.src) && a16(g.dst);
   if (!force_portable_v2()) {
     // hot (K, S) pairs: compile-time-K kernel with interior/edge warp ordering

@@ -30,10 +30,10 @@ namespace plgpu {
 
 constexpr int kNS3 = 4;
 
+// Per warp: NS staging chunks + one output chunk, R rows each.
 template <int ST, int LINES, bool ROWS>
 __host__ __device__ constexpr int pass3_smem_floats_per_warp() {
-  return kNS3 * (ST + 1) * (32 * LINES + (ROWS ? 2 : 0)) +
-         (ROWS ? (ST + 1) * (32 * LINES + 2) : 0);
+  return (kNS3 + 1) * (ST + 1) * (32 * LINES + (ROWS ? 2 : 0));
 }
 
 struct Pass3Desc {
@@ -73,25 +73,46 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
   auto slot = [&](int c) -> float* { return ring + (c & (kNS3 - 1)) * CHUNK; };
   // Copy chunk c (positions u = cR + BASE + q, q < R); always commits a group.
   // Positions with u < 0 (ahead of the anchor) are never read and not copied.
+  // Addresses advance incrementally (64-bit adds) from per-warp bases.
+  const int lane16 = lane & 15, half = lane >> 4;
+  const int64_t ps = g.src_pos_stride, ls = g.src_line_stride;
+  // ROWS: this lane copies lines l0 + 2j + half at positions q = lane16 (+16..)
+  const float* rows_base = src + (int64_t)min(l0 + half, last_line) * ls;
   auto issue_chunk = [&](int c) {
     if (c <= nchunks - 1) {
       float* dstc = slot(c);
       const int ubase = c * R + BASE;
       if constexpr (ROWS) {
-        // lanes 0..15 -> 16 consecutive positions of line 2j, lanes 16..31 -> line 2j+1
 #pragma unroll
         for (int qb = 0; qb < R; qb += 16) {
-          const int q = qb + (lane & 15);
+          const int q = qb + lane16;
           if (q < R && ubase + q >= 0) {
             const int p = pos0 + ubase + q;
-            const float* col = src + (int64_t)(EDGE ? mirror_pos(p, n) : p) * g.src_pos_stride;
-            float* drow = dstc + q * PITCH;
+            float* drow = dstc + q * PITCH + half;
+            if (EDGE || l0 + LW - 1 > last_line) {
+              const float* col = src + (int64_t)(EDGE ? mirror_pos(p, n) : p) * ps;
 #pragma unroll 4
-            for (int j = 0; j < LW / 2; ++j) {
-              const int l = 2 * j + (lane >> 4);
-              const int line = min(l0 + l, last_line);  // partial line groups
-              cp_async4(drow + l, col + (int64_t)line * g.src_line_stride);
+              for (int j = 0; j < LW / 2; ++j)
+                cp_async4(drow + 2 * j, col + (int64_t)min(l0 + 2 * j + half, last_line) * ls);
+            } else {
+              const float* gp = rows_base + p;
+#pragma unroll 8
+              for (int j = 0; j < LW / 2; ++j) {
+                cp_async4(drow + 2 * j, gp);
+                gp += 2 * ls;
+              }
             }
+          }
+        }
+      } else if (!EDGE && g.vec16) {
+        if (lane < LW / 4) {
+          const float* gp = src + (int64_t)(pos0 + ubase) * ps + l0 + 4 * lane;
+          float* dp = dstc + 4 * lane;
+#pragma unroll
+          for (int q = 0; q < R; ++q) {
+            if (ubase + q >= 0) cp_async16(dp, gp);
+            gp += ps;
+            dp += PITCH;
           }
         }
       } else {
@@ -99,14 +120,14 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
         for (int q = 0; q < R; ++q) {
           if (ubase + q < 0) continue;
           const int p = pos0 + ubase + q;
-          const float* rowp = src + (int64_t)(EDGE ? mirror_pos(p, n) : p) * g.src_pos_stride;
+          const float* rowp = src + (int64_t)(EDGE ? mirror_pos(p, n) : p) * ps;
           if (g.vec16) {
             if (lane < LW / 4) cp_async16(dstc + q * PITCH + 4 * lane, rowp + l0 + 4 * lane);
           } else {
 #pragma unroll
             for (int h = 0; h < LINES; ++h) {
               const int l = lane * LINES + h;
-              cp_async4(dstc + q * PITCH + l, rowp + (int64_t)min(l0 + l, last_line) * g.src_line_stride);
+              cp_async4(dstc + q * PITCH + l, rowp + (int64_t)min(l0 + l, last_line) * ls);
             }
           }
         }
@@ -157,7 +178,6 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
   const V one = Ops::splat(1.f);
   const int64_t dst_img = img * g.dst_img_stride;
   const int my_line = l0 + lane * LINES;
-  float* op = g.dst + dst_img + (int64_t)my_line * g.dst_line_stride + (int64_t)i0 * g.dst_pos_stride;
 
   for (int c = 0; c < nchunks; ++c) {
     __syncwarp();       // all lanes done with chunk c-2 (iteration c-1)
@@ -180,9 +200,6 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
       // so the scheduler overlaps consecutive steps.
       if (EDGE && s >= T) break;
       const int i = i0 + s;
-      const V tf = at(r, 2 + KT + ST);
-      const V tn = at(r, BASE);
-      const V to = at(r, 1 + ST);
       const V an_ = nr[r], ao = orr[r], fi = fr[r];
       const int kmax = EDGE ? min(S, n - 1 - i) : ST;
       V num = Ops::add(an[r], fi);
@@ -199,36 +216,58 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
         if constexpr (EDGE) w = Ops::zero_if(k > kmax, w);
         num = Ops::fma(w, fr[rk], num);
         den = Ops::add(w, den);
-        an[rk] = Ops::fma(w, fi, an[rk]);
-        ad[rk] = Ops::add(w, ad[rk]);
+        if (k == ST) {  // first contribution to the slot recycled at step r-1
+          an[rk] = Ops::fma(w, fi, zero);  // exactly the portable walker's fma(w, fi, 0)
+          ad[rk] = w;                      // == 0 + w (w >= +0)
+        } else {
+          an[rk] = Ops::fma(w, fi, an[rk]);
+          ad[rk] = Ops::add(w, ad[rk]);
+        }
       }
       const V qv = Ops::div(num, den);
       const float o0 = fminf(fmaxf(Ops::lo(qv), lo0), hi0);
       float o1 = o0;
       if constexpr (LINES == 2) o1 = fminf(fmaxf(Ops::hi(qv), lo1), hi1);
-      if constexpr (ROWS) {
+      {  // branch-free: every step lands in the output ring, filtered at the flush
         float* sl = oring + r * PITCH + lane * LINES;
         if constexpr (LINES == 2) *reinterpret_cast<float2*>(sl) = make_float2(o0, o1);
         else *sl = o0;
-      } else if (i >= s0) {
-        if constexpr (LINES == 2) {
-          if (g.vec16) {
-            *reinterpret_cast<float2*>(op) = make_float2(o0, o1);
-          } else {
-            if (my_line <= last_line) op[0] = o0;
-            if (my_line + 1 <= last_line) op[g.dst_line_stride] = o1;
+      }
+      // refill slot r in place: first read at step r+1's last offset
+      fr[r] = at(r, 2 + KT + ST);
+      nr[r] = at(r, BASE);
+      orr[r] = at(r, 1 + ST);
+      track(fr[r]);
+    }
+    if constexpr (!ROWS) {
+      // flush this iteration's outputs: row q = position i0 + sb + q, LW lines
+      __syncwarp();
+      if (g.vec16) {
+        constexpr int LPR = LW / 4;  // lanes per row, 16 B each
+#pragma unroll
+        for (int qb = 0; qb < R; qb += 32 / LPR) {
+          const int q = qb + lane / LPR;
+          const int p = i0 + sb + q;
+          if (q < R && p >= s0 && p < s1) {
+            const float4 v = *reinterpret_cast<const float4*>(oring + q * PITCH + 4 * (lane % LPR));
+            *reinterpret_cast<float4*>(g.dst + dst_img + (int64_t)p * g.dst_pos_stride + l0 +
+                                       4 * (lane % LPR)) = v;
           }
-        } else {
-          if (my_line <= last_line) *op = o0;
+        }
+      } else {
+#pragma unroll 2
+        for (int q = 0; q < R; ++q) {
+          const int p = i0 + sb + q;
+          if (p >= s0 && p < s1) {
+#pragma unroll
+            for (int h = 0; h < LINES; ++h)
+              if (my_line + h <= last_line)
+                g.dst[dst_img + (int64_t)p * g.dst_pos_stride + (int64_t)(my_line + h) * g.dst_line_stride] =
+                    oring[q * PITCH + lane * LINES + h];
+          }
         }
       }
-      if constexpr (!ROWS) op += g.dst_pos_stride;
-      an[r] = zero;
-      ad[r] = zero;
-      track(tf);
-      fr[r] = tf;
-      nr[r] = tn;
-      orr[r] = to;
+      __syncwarp();
     }
     if constexpr (ROWS) {
       // flush this iteration's outputs: positions p = i0 + sb + q, q < R
@@ -241,16 +280,26 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
           const int blk = g.dst_pos_block;
           const int64_t pofs =
               (int64_t)(p / blk) * g.dst_block_stride + (int64_t)(p % blk) * g.dst_pos_stride;
-          float* dbase = g.dst + dst_img + pofs;
-          const float* orow = oring + q * PITCH;
+          const float* orow = oring + q * PITCH + half;
+          if (l0 + LW - 1 <= last_line) {
+            float* dp = g.dst + dst_img + pofs + (int64_t)(l0 + half) * g.dst_line_stride;
+            const int64_t dstep = 2 * g.dst_line_stride;
+#pragma unroll 8
+            for (int j = 0; j < LW / 2; ++j) {
+              *dp = orow[2 * j];
+              dp += dstep;
+            }
+          } else {
+            float* dbase = g.dst + dst_img + pofs;
 #pragma unroll 4
-          for (int j = 0; j < LW / 2; ++j) {
-            const int l = 2 * j + (lane >> 4);
-            if (l0 + l <= last_line)
-              dbase[(int64_t)(l0 + l) * g.dst_line_stride] = orow[l];
+            for (int j = 0; j < LW / 2; ++j) {
+              const int l = 2 * j + half;
+              if (l0 + l <= last_line) dbase[(int64_t)(l0 + l) * g.dst_line_stride] = orow[2 * j];
+            }
           }
         }
       }
+      __syncwarp();
     }
   }
   cp_wait<0>();

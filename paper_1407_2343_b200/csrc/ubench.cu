@@ -6,6 +6,8 @@
 
 #include <cstdint>
 
+#include "plgpu_walk2.cuh"
+
 namespace {
 
 constexpr int kChains = 8;
@@ -67,9 +69,125 @@ __global__ void ffma2_kernel(float* out, int iters, float a, float b) {
   if (s == 1.2345f) out[threadIdx.x] = s;
 }
 
+// The walker's per-pair update on register-resident data (no rings, no
+// memory): LINES=2 packed form.  NK independent offsets per step; every
+// accumulation pattern of the real kernel is kept (two num/den chains).
+template <int NK>
+__global__ void pair2_kernel(float* out, int iters, float c) {
+  using O = plgpu::VecOps<2>;
+  using V = O::V;
+  V p[NK + 1], q[NK + 1], f[NK + 1], d[NK + 1], an[NK + 1], ad[NK + 1];
+#pragma unroll
+  for (int k = 0; k <= NK; ++k) {
+    p[k] = O::splat(threadIdx.x * 0.001f + k);
+    q[k] = O::splat(threadIdx.x * 0.002f + k);
+    f[k] = O::splat(k * 1.5f);
+    d[k] = O::splat(0.f);
+    an[k] = O::splat(0.f);
+    ad[k] = O::splat(0.f);
+  }
+  const V cv = O::splat(c), one = O::splat(1.f);
+  V num = O::splat(0.f), den = O::splat(0.f);
+  for (int it = 0; it < iters; ++it) {
+    const V a = p[it & 1 ? 0 : NK], b = q[it & 1 ? 0 : NK], fi = f[0];
+    num = O::add(num, fi);
+    den = O::add(den, one);
+#pragma unroll
+    for (int k = 1; k <= NK; ++k) {
+      const V dn = O::sub(a, p[k]);
+      V dk = O::fma(dn, dn, d[k]);
+      const V dq = O::sub(b, q[k]);
+      dk = O::fms(dq, dq, dk);
+      d[k] = dk;
+      const V w = O::ex2(O::mul(dk, cv));
+      num = O::fma(w, f[k], num);
+      den = O::add(w, den);
+      an[k] = O::fma(w, fi, an[k]);
+      ad[k] = O::add(w, ad[k]);
+    }
+  }
+  float s = O::lo(num) + O::hi(den);
+#pragma unroll
+  for (int k = 1; k <= NK; ++k) s += O::lo(an[k]) + O::hi(ad[k]) + O::lo(d[k]);
+  if (s == c) out[threadIdx.x] = s;
+}
+
+// LINES=1 form with {num, den} packed in one f32x2 accumulator:
+// {num, den} += w * {f, 1} is ONE FFMA2 (w broadcast).
+template <int NK>
+__global__ void pair1_kernel(float* out, int iters, float c) {
+  using O2 = plgpu::VecOps<2>;
+  using V2 = O2::V;
+  float p[NK + 1], q[NK + 1], d[NK + 1];
+  V2 f1[NK + 1], acc[NK + 1];
+#pragma unroll
+  for (int k = 0; k <= NK; ++k) {
+    p[k] = threadIdx.x * 0.001f + k;
+    q[k] = threadIdx.x * 0.002f + k;
+    f1[k] = plgpu::f2_make(k * 1.5f, 1.f);
+    d[k] = 0.f;
+    acc[k] = O2::splat(0.f);
+  }
+  V2 nd = O2::splat(0.f);
+  for (int it = 0; it < iters; ++it) {
+    const float a = p[it & 1 ? 0 : NK], b = q[it & 1 ? 0 : NK];
+    const V2 fi = f1[0];
+    nd = O2::add(nd, fi);
+#pragma unroll
+    for (int k = 1; k <= NK; ++k) {
+      const float dn = a - p[k];
+      float dk = fmaf(dn, dn, d[k]);
+      const float dq = b - q[k];
+      dk = fmaf(-dq, dq, dk);
+      d[k] = dk;
+      const float w = plgpu::ex2_approx(dk * c);
+      const V2 wv = O2::splat(w);
+      nd = O2::fma(wv, f1[k], nd);
+      acc[k] = O2::fma(wv, fi, acc[k]);
+    }
+  }
+  float s = O2::lo(nd) + O2::hi(nd);
+#pragma unroll
+  for (int k = 1; k <= NK; ++k) s += O2::lo(acc[k]) + O2::hi(acc[k]) + d[k];
+  if (s == c) out[threadIdx.x] = s;
+}
+
 }  // namespace
 
 extern "C" {
+
+// Pair-update throughput: unique pairs per second (each lane-line-offset is
+// one pair).  form 0: LINES=2 packed; form 1: LINES=1 with {num,den} packed.
+double plub_pair_rate(int form, int blocks_per_sm, int threads, int iters, double* ms_out) {
+  int dev = 0, sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  float* out = nullptr;
+  if (cudaMalloc(&out, 4096 * sizeof(float)) != cudaSuccess) return -1;
+  const int blocks = sms * blocks_per_sm;
+  constexpr int NK = 10;
+  auto launch = [&]() {
+    if (form == 0) pair2_kernel<NK><<<blocks, threads>>>(out, iters, -1e-4f);
+    else pair1_kernel<NK><<<blocks, threads>>>(out, iters, -1e-4f);
+  };
+  launch();
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  for (int r = 0; r < 3; ++r) launch();
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(out);
+  if (cudaGetLastError() != cudaSuccess) return -1;
+  const double pairs = (form == 0 ? 2.0 : 1.0) * NK * (double)iters * blocks * threads * 3;
+  if (ms_out) *ms_out = ms / 3;
+  return pairs / (ms * 1e-3);
+}
 
 // Returns lane-operations per second (ex2: exps/s; ffma: FMAs/s; ffma2: FMAs/s
 // counting 2 per packed instruction) and the measured milliseconds; -1 on error.

@@ -1,0 +1,22 @@
+"""Pipe-throughput microbenchmarks on the GPU box (lib/libplubench.so)."""
+import ctypes as C
+import json
+import os
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+L = C.CDLL(os.path.join(ROOT, "paper_1407_2343_b200", "lib", "libplubench.so"))
+for fn in (L.plub_rate, L.plub_pair_rate):
+    fn.restype = C.c_double
+    fn.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]
+import torch  # noqa: E402  (initialises the device)
+torch.cuda.init()
+ms = C.c_double(0)
+res = {}
+for name, w in (("ex2", 0), ("ffma", 1), ("ffma2", 2)):
+    res[name + "_per_s"] = L.plub_rate(w, 8, 256, 4096, C.byref(ms))
+for form in (0, 1):
+    for bps, thr in ((2, 64), (4, 64), (6, 64), (8, 64), (4, 128), (8, 128), (16, 64)):
+        r = L.plub_pair_rate(form, bps, thr, 2000, C.byref(ms))
+        res[f"pair_form{form}_b{bps}_t{thr}"] = r
+res["ex2_frac"] = {k: v / res["ex2_per_s"] for k, v in res.items() if k.startswith("pair")}
+print(json.dumps(res, indent=1))
