@@ -85,6 +85,17 @@ bool force_portable() {
   }();
   return f;
 }
+// Lines per lane of the hot-configuration kernel: 1 = one line per lane with
+// {num, den} packed, 2 = two lines per lane packed line-wise.
+int walk3_lines(int ST) {
+  static const int forced = [] {
+    const char* e = std::getenv("PLGPU_LINES");
+    return (e && (e[0] == '1' || e[0] == '2')) ? e[0] - '0' : 0;
+  }();
+  if (ST > 16) return 1;
+  if (forced) return forced;
+  return ST <= 10 ? 2 : 1;  // measured on B200: c4 (S=10) 2 lines, c3 (S=15) 1 line
+}
 // PLGPU_FORCE_WALKER=2 skips only the hot-configuration kernel (walk3).
 bool force_portable_v2() {
   static const bool f = [] {
@@ -198,6 +209,14 @@ int try_pass2(const plgpu::PassDesc& g, cudaStream_t st) {
       const int R = ST + 1, BASE = ST + 2 * KT3 + 2;
       plgpu::Pass3Desc d3{};
       d3.b = d;
+      // lines per lane for the hot kernel (PLGPU_LINES=1|2 overrides)
+      d3.lines = walk3_lines(ST);
+      const int LW3 = 32 * d3.lines;
+      d3.b.groups_per_img = (g.lines_per_img + LW3 - 1) / LW3;
+      d3.b.total_warps = images * d3.b.groups_per_img * d.nseg;
+      d3.b.vec16 = !rows && g.lines_per_img % LW3 == 0 && g.src_pos_stride % 4 == 0 &&
+                   g.src_img_stride % 4 == 0 && g.dst_pos_stride % 4 == 0 &&
+                   g.dst_img_stride % 4 == 0 && a16(g.src) && a16(g.dst);
       int lo = d.nseg, hi = -1;
       for (int sgi = 0; sgi < d.nseg; ++sgi) {
         const int s0 = sgi * d.seg_len, s1 = std::min(d.n, s0 + d.seg_len);
@@ -215,7 +234,7 @@ int try_pass2(const plgpu::PassDesc& g, cudaStream_t st) {
       }
       d3.seg_lo = lo;
       d3.seg_hi = hi;
-      const int64_t groups = d.total_warps / d.nseg;
+      const int64_t groups = d3.b.total_warps / d.nseg;
       d3.interior_warps = groups * std::max(0, hi - lo + 1);
       bool launched = false;
       switch (ST) {

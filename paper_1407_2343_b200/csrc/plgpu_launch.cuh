@@ -6,6 +6,8 @@
 
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include "plgpu_walk.cuh"
 #include "plgpu_walk2.cuh"
 #include "plgpu_walk3.cuh"
@@ -78,14 +80,22 @@ bool launch_pass3(const Pass3Desc& d, bool rows, cudaStream_t st) {
     return false;
   } else {
     if (d.b.K != KT || d.b.S != ST) return false;
-    constexpr int L = pass2_lines(ST);
     const unsigned blocks = (unsigned)((d.b.total_warps + kWarpsPerCta - 1) / kWarpsPerCta);
-    if (rows) {
-      const size_t smem = sizeof(float) * kWarpsPerCta * pass3_smem_floats_per_warp<ST, L, true>();
-      nlm_pass3_kernel<ST, KT, L, true><<<blocks, 32 * kWarpsPerCta, smem, st>>>(d);
+    auto go = [&](auto lines_tag) {
+      constexpr int L = decltype(lines_tag)::value;
+      if (rows) {
+        const size_t smem = sizeof(float) * kWarpsPerCta * pass3_smem_floats_per_warp<ST, L, true>();
+        nlm_pass3_kernel<ST, KT, L, true><<<blocks, 32 * kWarpsPerCta, smem, st>>>(d);
+      } else {
+        const size_t smem = sizeof(float) * kWarpsPerCta * pass3_smem_floats_per_warp<ST, L, false>();
+        nlm_pass3_kernel<ST, KT, L, false><<<blocks, 32 * kWarpsPerCta, smem, st>>>(d);
+      }
+    };
+    if constexpr (ST <= 16) {
+      if (d.lines == 2) go(std::integral_constant<int, 2>{});
+      else go(std::integral_constant<int, 1>{});
     } else {
-      const size_t smem = sizeof(float) * kWarpsPerCta * pass3_smem_floats_per_warp<ST, L, false>();
-      nlm_pass3_kernel<ST, KT, L, false><<<blocks, 32 * kWarpsPerCta, smem, st>>>(d);
+      go(std::integral_constant<int, 1>{});
     }
     return true;
   }

@@ -38,6 +38,7 @@ __host__ __device__ constexpr int pass3_smem_floats_per_warp() {
 
 struct Pass3Desc {
   Pass2Desc b;          // geometry (strides, lines, segments, coef, S, K)
+  int32_t lines;        // lines per lane (1 or 2); b.total_warps / groups follow it
   int32_t seg_lo, seg_hi;  // interior segment range [seg_lo, seg_hi]
   int64_t interior_warps;  // groups * (seg_hi - seg_lo + 1)
 };
@@ -145,8 +146,16 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
     const int c = (u - BASE + M * R) / R - M;  // floor((u - BASE) / R)
     return Ops::lds(slot(c) + (u - BASE - c * R) * PITCH + lane * LINES);
   };
-  V fr[R], nr[R], orr[R], an[R], ad[R], d[R];
+  // LINES == 2: two lines per lane, all state packed line-wise (f32x2).
+  // LINES == 1: one line per lane; the numerator/denominator pairs are packed
+  // instead, {num, den} += w * {f, 1} being one FFMA2 (w broadcast), and the
+  // f ring holds {f, 1} pairs.  Same per-line arithmetic either way.
+  constexpr bool PK = LINES == 1;
+  V fr[PK ? 1 : R], an[PK ? 1 : R], ad[PK ? 1 : R];
+  V nr[R], orr[R], d[R];
+  F2 frp[PK ? R : 1], acc[PK ? R : 1];
   const V zero = Ops::splat(0.f);
+  const F2 zero2 = f2_make(0.f, 0.f);
   float lo0 = 3.402823466e38f, hi0 = -3.402823466e38f, lo1 = lo0, hi1 = hi0;
   auto track = [&](V v) {
     lo0 = fminf(lo0, Ops::lo(v));
@@ -156,13 +165,19 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
   };
 #pragma unroll
   for (int q = 0; q < R; ++q) {
-    fr[q] = ld_init(q + 1 + KT);
     nr[q] = ld_init(q + 1 + 2 * KT);
     orr[q] = ld_init(q);
-    an[q] = zero;
-    ad[q] = zero;
     d[q] = zero;
-    track(fr[q]);
+    const V f = ld_init(q + 1 + KT);
+    if constexpr (PK) {
+      frp[q] = f2_make(Ops::lo(f), 1.f);
+      acc[q] = zero2;
+    } else {
+      fr[q] = f;
+      an[q] = zero;
+      ad[q] = zero;
+    }
+    track(f);
   }
 #pragma unroll
   for (int t = 0; t <= 2 * KT; ++t) {  // anchor d_k(i0-1), t ascending
@@ -200,31 +215,57 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
       // so the scheduler overlaps consecutive steps.
       if (EDGE && s >= T) break;
       const int i = i0 + s;
-      const V an_ = nr[r], ao = orr[r], fi = fr[r];
+      const V an_ = nr[r], ao = orr[r];
       const int kmax = EDGE ? min(S, n - 1 - i) : ST;
-      V num = Ops::add(an[r], fi);
-      V den = Ops::add(ad[r], one);
+      V qv;
+      if constexpr (PK) {
+        using O2 = VecOps<2>;
+        const F2 fip = frp[r];
+        F2 nd = O2::add(acc[r], fip);  // {j-side num + f_i, j-side den + 1}
 #pragma unroll
-      for (int k = 1; k <= ST; ++k) {
-        const int rk = (r + k) % R;
-        const V dn = Ops::sub(an_, nr[rk]);
-        V dk = Ops::fma(dn, dn, d[k]);
-        const V dq = Ops::sub(ao, orr[rk]);
-        dk = Ops::fms(dq, dq, dk);
-        d[k] = dk;
-        V w = Ops::ex2(Ops::mul(dk, coefv));
-        if constexpr (EDGE) w = Ops::zero_if(k > kmax, w);
-        num = Ops::fma(w, fr[rk], num);
-        den = Ops::add(w, den);
-        if (k == ST) {  // first contribution to the slot recycled at step r-1
-          an[rk] = Ops::fma(w, fi, zero);  // exactly the portable walker's fma(w, fi, 0)
-          ad[rk] = w;                      // == 0 + w (w >= +0)
-        } else {
-          an[rk] = Ops::fma(w, fi, an[rk]);
-          ad[rk] = Ops::add(w, ad[rk]);
+        for (int k = 1; k <= ST; ++k) {
+          const int rk = (r + k) % R;
+          const float dn = an_ - nr[rk];
+          float dk = fmaf(dn, dn, d[k]);
+          const float dq = ao - orr[rk];
+          dk = fmaf(-dq, dq, dk);
+          d[k] = dk;
+          float w = ex2_approx(dk * g.coef);
+          if constexpr (EDGE) w = k > kmax ? 0.f : w;
+          const F2 ww = f2_make(w, w);
+          nd = O2::fma(frp[rk], ww, nd);  // num += w f_{i+k}; den += w
+          // first contribution to the slot recycled at step r-1: fma with 0
+          acc[rk] = O2::fma(fip, ww, k == ST ? zero2 : acc[rk]);
         }
+        float qn, qd;
+        f2_split(nd, qn, qd);
+        qv = div_fix(qn, qd);
+      } else {
+        const V fi = fr[r];
+        V num = Ops::add(an[r], fi);
+        V den = Ops::add(ad[r], one);
+#pragma unroll
+        for (int k = 1; k <= ST; ++k) {
+          const int rk = (r + k) % R;
+          const V dn = Ops::sub(an_, nr[rk]);
+          V dk = Ops::fma(dn, dn, d[k]);
+          const V dq = Ops::sub(ao, orr[rk]);
+          dk = Ops::fms(dq, dq, dk);
+          d[k] = dk;
+          V w = Ops::ex2(Ops::mul(dk, coefv));
+          if constexpr (EDGE) w = Ops::zero_if(k > kmax, w);
+          num = Ops::fma(w, fr[rk], num);
+          den = Ops::add(w, den);
+          if (k == ST) {  // first contribution to the slot recycled at step r-1
+            an[rk] = Ops::fma(w, fi, zero);  // exactly the portable walker's fma(w, fi, 0)
+            ad[rk] = w;                      // == 0 + w (w >= +0)
+          } else {
+            an[rk] = Ops::fma(w, fi, an[rk]);
+            ad[rk] = Ops::add(w, ad[rk]);
+          }
+        }
+        qv = Ops::div(num, den);
       }
-      const V qv = Ops::div(num, den);
       const float o0 = fminf(fmaxf(Ops::lo(qv), lo0), hi0);
       float o1 = o0;
       if constexpr (LINES == 2) o1 = fminf(fmaxf(Ops::hi(qv), lo1), hi1);
@@ -234,10 +275,12 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
         else *sl = o0;
       }
       // refill slot r in place: first read at step r+1's last offset
-      fr[r] = at(r, 2 + KT + ST);
+      const V fnew = at(r, 2 + KT + ST);
+      if constexpr (PK) frp[r] = f2_make(Ops::lo(fnew), 1.f);
+      else fr[r] = fnew;
       nr[r] = at(r, BASE);
       orr[r] = at(r, 1 + ST);
-      track(fr[r]);
+      track(fnew);
     }
     if constexpr (!ROWS) {
       // flush this iteration's outputs: row q = position i0 + sb + q, LW lines

@@ -88,8 +88,12 @@ __global__ void pair2_kernel(float* out, int iters, float c) {
   }
   const V cv = O::splat(c), one = O::splat(1.f);
   V num = O::splat(0.f), den = O::splat(0.f);
+  V a = p[0], b = q[0];
+  const V drift = O::splat(1e-7f);
   for (int it = 0; it < iters; ++it) {
-    const V a = p[it & 1 ? 0 : NK], b = q[it & 1 ? 0 : NK], fi = f[0];
+    a = O::add(a, drift);
+    b = O::add(b, drift);
+    const V fi = f[0];
     num = O::add(num, fi);
     den = O::add(den, one);
 #pragma unroll
@@ -129,8 +133,10 @@ __global__ void pair1_kernel(float* out, int iters, float c) {
     acc[k] = O2::splat(0.f);
   }
   V2 nd = O2::splat(0.f);
+  float a = p[0], b = q[0];
   for (int it = 0; it < iters; ++it) {
-    const float a = p[it & 1 ? 0 : NK], b = q[it & 1 ? 0 : NK];
+    a += 1e-7f;
+    b += 1e-7f;
     const V2 fi = f1[0];
     nd = O2::add(nd, fi);
 #pragma unroll
@@ -152,9 +158,78 @@ __global__ void pair1_kernel(float* out, int iters, float c) {
   if (s == c) out[threadIdx.x] = s;
 }
 
+// Packed-op throughput with full register-pair operands (no broadcast):
+// op 0: FFMA2 a*b+c (3 pairs), 1: FADD2 a+b (2 pairs), 2: FMUL2 a*b,
+// 3: FFMA2 + FADD2 alternating, 4: scalar FFMA 3 regs, 5: scalar FADD.
+template <int OP>
+__global__ void pk_kernel(float* out, int iters) {
+  using O = plgpu::VecOps<2>;
+  using V = O::V;
+  constexpr int NC = 8;
+  V x[NC], y[NC];
+  float xs[NC], ys[NC];
+#pragma unroll
+  for (int k = 0; k < NC; ++k) {
+    x[k] = plgpu::f2_make(threadIdx.x * 1e-3f + k, k * 0.5f);
+    y[k] = plgpu::f2_make(0.999f - k * 1e-4f, 1.0001f + k * 1e-5f);
+    xs[k] = threadIdx.x * 1e-3f + k;
+    ys[k] = 0.999f - k * 1e-4f;
+  }
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+      const int j = (k + 3) % NC;
+      if (OP == 0) x[k] = O::fma(x[k], y[k], x[j]);
+      if (OP == 1) x[k] = O::add(x[k], y[j]);
+      if (OP == 2) x[k] = O::mul(x[k], y[j]);
+      if (OP == 3) { x[k] = (k & 1) ? O::add(x[k], y[j]) : O::fma(x[k], y[k], x[j]); }
+      if (OP == 4) xs[k] = fmaf(xs[k], ys[k], xs[j]);
+      if (OP == 5) xs[k] = xs[k] + ys[j];
+    }
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < NC; ++k) s += O::lo(x[k]) + O::hi(x[k]) + xs[k];
+  if (s == 1.2345f) out[threadIdx.x] = s;
+}
+
 }  // namespace
 
 extern "C" {
+
+// Warp-instructions per second per SM for pk_kernel<op>.
+double plub_pk_rate(int op, int blocks_per_sm, int threads, int iters) {
+  int dev = 0, sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  float* out = nullptr;
+  if (cudaMalloc(&out, 4096 * sizeof(float)) != cudaSuccess) return -1;
+  const int blocks = sms * blocks_per_sm;
+  auto launch = [&]() {
+    switch (op) {
+      case 0: pk_kernel<0><<<blocks, threads>>>(out, iters); break;
+      case 1: pk_kernel<1><<<blocks, threads>>>(out, iters); break;
+      case 2: pk_kernel<2><<<blocks, threads>>>(out, iters); break;
+      case 3: pk_kernel<3><<<blocks, threads>>>(out, iters); break;
+      case 4: pk_kernel<4><<<blocks, threads>>>(out, iters); break;
+      default: pk_kernel<5><<<blocks, threads>>>(out, iters); break;
+    }
+  };
+  launch();
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  for (int r = 0; r < 3; ++r) launch();
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaFree(out);
+  if (cudaGetLastError() != cudaSuccess) return -1;
+  const double warp_instr = 8.0 * iters * (double)blocks * (threads / 32) * 3;
+  return warp_instr / (ms * 1e-3) / sms;
+}
 
 // Pair-update throughput: unique pairs per second (each lane-line-offset is
 // one pair).  form 0: LINES=2 packed; form 1: LINES=1 with {num,den} packed.

@@ -20,3 +20,12 @@ for form in (0, 1):
         res[f"pair_form{form}_b{bps}_t{thr}"] = r
 res["ex2_frac"] = {k: v / res["ex2_per_s"] for k, v in res.items() if k.startswith("pair")}
 print(json.dumps(res, indent=1))
+L.plub_pk_rate.restype = C.c_double
+L.plub_pk_rate.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int]
+clk = 1.965e9
+pk = {}
+for op, name in enumerate(["ffma2_3pair", "fadd2_2pair", "fmul2_2pair", "ffma2_fadd2_mix", "ffma_3reg", "fadd_2reg"]):
+    for bps, thr in ((4, 128), (8, 128)):
+        r = L.plub_pk_rate(op, bps, thr, 4000)
+        pk[f"{name}_w{bps*thr//32}"] = {"warp_instr_per_clk_per_sm": r / clk, "cycles_per_instr_per_smsp": 4 * clk / r}
+print(json.dumps(pk, indent=1))
