@@ -70,11 +70,19 @@ def shard(n_items: int, world: int, rank: int):
     return lo, hi
 
 
-def make_inputs(cfg_name, lo, hi):
+def slab_mode(cfg_name, world):
+    """c5 at N > 1: one image, row slabs -> all-to-all -> column slabs."""
+    return cfg_name == "c5" and world > 1
+
+
+def make_inputs(cfg_name, lo, hi, row_range=None):
     from paper_1407_2343_b200 import workloads as W
     c = W.CONFIGS[cfg_name]
     if c["kind"] == "signal":
         return W.make_signal(c["n"], c["sigma"], seed=1)[None, :]
+    if row_range is not None:
+        return W.make_image(c["rows"], c["cols"], c["shapes"], c["sigma"], seed=1 * 1000003,
+                            quantize=c.get("quantize", False), row_range=row_range)[None]
     out = np.empty((hi - lo, c["rows"], c["cols"]), np.float32)
     for k, b in enumerate(range(lo, hi)):
         out[k] = W.make_image(c["rows"], c["cols"], c["shapes"], c["sigma"], seed=1 * 1000003 + b,
@@ -270,23 +278,47 @@ def run_ours(args):
     c, S, K, h = workload(args.config)
     params = (S, K, h)
     n_items = c.get("batch", 1)
-    if c["kind"] == "signal":
+    slab = slab_mode(args.config, world)
+    if c["kind"] == "signal" or slab:
         lo, hi = 0, 1
     else:
         lo, hi = shard(n_items, world, rank)
-    imgs_host = make_inputs(args.config, lo, hi)
+    if slab:
+        from paper_1407_2343_b200.distributed import SlabPlan
+        plan = SlabPlan(c["rows"], c["cols"], world, rank)
+        imgs_host = make_inputs(args.config, 0, 1, row_range=plan.rows)
+    else:
+        imgs_host = make_inputs(args.config, lo, hi)
     x = torch.from_numpy(imgs_host).to(dev)
     y = torch.empty_like(x)
     mid = torch.empty_like(x)
     stream = torch.cuda.current_stream()
     signal = c["kind"] == "signal"
+    if slab:
+        cb = c["cols"] // world
+        recv = torch.empty_like(x)
+        y = torch.empty((c["rows"], cb), dtype=x.dtype, device=dev)
 
-    def step():
+    def first_pass():
         if signal:
             pl.nlm_1d_patchlift(x, params, out=y)
+        elif slab:
+            pl.nlm_row_pass_blocked(x, params, cb, out=mid)
+            torch.distributed.all_to_all_single(recv.reshape(-1), mid.reshape(-1))
+        else:
+            pl.nlm_row_pass(x, params, out=mid)
+
+    def second_pass():
+        if signal:
             return
-        pl.nlm_row_pass(x, params, out=mid)
-        pl.nlm_col_pass(mid, params, out=y)
+        if slab:
+            pl.nlm_col_pass(recv.reshape(c["rows"], cb), params, out=y)
+        else:
+            pl.nlm_col_pass(mid, params, out=y)
+
+    def step():
+        first_pass()
+        second_pass()
 
     for _ in range(max(3, args.warmup)):
         step()
@@ -303,13 +335,9 @@ def run_ours(args):
         start.record(stream)
         for k in range(args.steps):
             ev[k][0].record(stream)
-            if signal:
-                pl.nlm_1d_patchlift(x, params, out=y)
-                ev[k][1].record(stream)
-            else:
-                pl.nlm_row_pass(x, params, out=mid)
-                ev[k][1].record(stream)
-                pl.nlm_col_pass(mid, params, out=y)
+            first_pass()
+            ev[k][1].record(stream)
+            second_pass()
             ev[k][2].record(stream)
         end.record(stream)
         torch.cuda.synchronize()
@@ -330,6 +358,9 @@ def run_ours(args):
     if signal:
         px_local = c["n"]
         px_total = px_local
+    elif slab:
+        px_local = c["rows"] * c["cols"] // world
+        px_total = c["rows"] * c["cols"]
     else:
         px_local = (hi - lo) * c["rows"] * c["cols"]
         px_total = n_items * c["rows"] * c["cols"]
@@ -339,6 +370,9 @@ def run_ours(args):
     if signal:
         u_row = pl.unique_pairs(c["n"], S)
         u_col = 0
+    elif slab:
+        u_row = (c["rows"] // world) * pl.unique_pairs(c["cols"], S)
+        u_col = (c["cols"] // world) * pl.unique_pairs(c["rows"], S)
     else:
         u_row = (hi - lo) * c["rows"] * pl.unique_pairs(c["cols"], S)
         u_col = (hi - lo) * c["cols"] * pl.unique_pairs(c["rows"], S)
@@ -350,25 +384,31 @@ def run_ours(args):
     ex2_peak, ffma_peak = (mufu_peak() if rank == 0 else (None, None))
     f_max = peaks.get("sm_max_mhz", 1965.0) * 1e6
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
-    nominal = 16 * sms * f_max
+    # Roofline of SURVEY.md sec. 8(d): per unique pair 1 MUFU.EX2 + 8 FP32 lane-ops,
+    # per pass 8 HBM bytes per pixel.  Peaks measured live on this GPU
+    # (lib/libplubench.so); nominal: 16 ex2 and 128 FP32 lanes per clock per SM.
+    ex2_rate = ex2_peak or 16 * sms * f_max
+    fp32_rate = ffma_peak or 128 * sms * f_max
+    pair_peak = min(ex2_rate, fp32_rate / 8.0)  # pairs/s
     achieved = u_dom / (t_dom * 1e-3)
-    peak = ex2_peak or nominal
     hbm_bytes = 8 * px_local  # per pass: fp32 read + write
+    hbm_gbs = peaks.get("hbm_gbs", 6541.5)
     roof = {
-        "bound": "sfu", "achieved": achieved / 1e9, "peak": peak / 1e9, "unit": "Gexp/s",
-        "frac": achieved / peak, "traffic": ncu_traffic(args.config),
-        "kernel": f"nlm_pass_kernel ({dom} pass)",
-        "peak_source": "live MUFU.EX2 microbenchmark (lib/libplubench.so)" if ex2_peak
-        else f"nominal 16/clk/SM x {sms} SM x {f_max / 1e6:.0f} MHz",
-        "peak_nominal": nominal / 1e9,
-        "frac_of_nominal": achieved / nominal,
-        "algorithmic_per_launch": {"exps": u_dom, "hbm_bytes": hbm_bytes},
+        "bound": "fp32" if fp32_rate / 8.0 < ex2_rate else "sfu",
+        "achieved": achieved / 1e9, "peak": pair_peak / 1e9, "unit": "Gpair/s",
+        "frac": achieved / pair_peak, "traffic": ncu_traffic(args.config),
+        "kernel": f"nlm_pass3_kernel ({dom} pass)",
+        "definition": "unique in-band pairs U per launch / CUDA-event launch time; peak = "
+                      "min(MUFU.EX2 rate, FP32 lane-op rate / 8), both measured live",
+        "ex2_peak_gexp_s": ex2_rate / 1e9, "fp32_peak_glaneops_s": fp32_rate / 1e9,
+        "frac_of_ex2": achieved / ex2_rate,
+        "peak_nominal_gpair_s": 16 * sms * f_max / 1e9,
+        "algorithmic_per_launch": {"pairs": u_dom, "exps": u_dom, "fp32_ops": 8 * u_dom,
+                                   "hbm_bytes": hbm_bytes},
         "row_pass_ms": row_avg, "col_pass_ms": col_avg,
-        "step_frac": (u_row + u_col) / (ms_step * 1e-3) / peak,
-        "hbm": {"achieved_gbs": hbm_bytes / (t_dom * 1e-3) / 1e9, "peak_gbs": peaks.get("hbm_gbs"),
-                "t_hbm_ms": hbm_bytes / (peaks.get("hbm_gbs", 6541.5) * 1e9) * 1e3},
-        "ffma_peak_gflops_measured": (ffma_peak / 1e9) if ffma_peak else None,
-        "ffma2_peak_gflops_measured": (getattr(mufu_peak, "ffma2", None) or 0) / 1e9 or None,
+        "step_frac": (u_row + u_col) / (ms_step * 1e-3) / pair_peak,
+        "hbm": {"achieved_gbs": hbm_bytes / (t_dom * 1e-3) / 1e9, "peak_gbs": hbm_gbs,
+                "t_hbm_ms": hbm_bytes / (hbm_gbs * 1e9) * 1e3},
     }
 
     line = None
@@ -388,7 +428,28 @@ def run_ours(args):
         }
 
     # ---- e2e through the C-ABI host entry point (N GPUs: each rank its shard) --
-    if not signal:
+    if slab:
+        hin = torch.from_numpy(imgs_host).pin_memory()
+        hout = torch.empty((c["rows"], cb), dtype=torch.float32).pin_memory()
+        torch.cuda.synchronize()
+        torch.distributed.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            x.copy_(hin, non_blocking=True)
+            step()
+            hout.copy_(y, non_blocking=True)
+            torch.cuda.synchronize()
+        e2e_s = (time.perf_counter() - t0) / args.e2e_steps
+        te = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
+        if rank == 0:
+            line["e2e"] = {"value": px_total / float(te.item()) / 1e6, "unit": UNIT,
+                           "h2d_bytes_per_step": int(hin.numel() * 4) * world,
+                           "d2h_bytes_per_step": int(hout.numel() * 4) * world,
+                           "api": "pinned H2D + row pass + NCCL all-to-all + column pass + D2H"}
+            line["config"]["nvlink_bytes_per_rank"] = plan.nvlink_bytes()
+            line["config"]["parallelism"] = f"row slabs -> all-to-all -> column slabs x{world}"
+    elif not signal:
         hin = torch.from_numpy(imgs_host).pin_memory()
         hout = torch.empty_like(hin).pin_memory()
         pl.snlm_2d_row_col_host(hin, params, hout)  # warm-up

@@ -54,20 +54,26 @@ def make_signal(n: int = 65536, sigma: float = 20.0, seed: int = 1, segments: in
     return x.astype(np.float32)
 
 
+NOISE_BLOCK = 256  # rows per independently seeded noise block
+
+
 def make_image(rows: int, cols: int, shapes: int, sigma: float, seed: int = 1,
-               quantize: bool = False) -> np.ndarray:
+               quantize: bool = False, row_range: tuple[int, int] | None = None) -> np.ndarray:
+    """Synthetic image (or only its rows [r0, r1) -- identical values either way,
+    so a rank can build just its row slab)."""
+    r0, r1 = row_range if row_range is not None else (0, rows)
     rng = np.random.Generator(np.random.PCG64(seed))
-    r = np.arange(rows, dtype=np.float32)[:, None]
+    r = np.arange(r0, r1, dtype=np.float32)[:, None]
     c = np.arange(cols, dtype=np.float32)[None, :]
     img = (32.0 + 192.0 * (r + c) / max(1, rows + cols - 2)).astype(np.float32)
-    img = np.broadcast_to(img, (rows, cols)).copy()
+    img = np.broadcast_to(img, (r1 - r0, cols)).copy()
     lo, hi = max(1.0, rows / 64.0), max(1.0, rows / 8.0)
     for _ in range(shapes):
         cy, cx = rng.uniform(0, rows), rng.uniform(0, cols)
         size = rng.uniform(lo, hi)
         val = np.float32(rng.uniform(0.0, 255.0))
         disk = rng.uniform() < 0.5
-        y0, y1 = max(0, int(cy - size)), min(rows, int(math.ceil(cy + size)) + 1)
+        y0, y1 = max(r0, int(cy - size)), min(r1, int(math.ceil(cy + size)) + 1)
         x0, x1 = max(0, int(cx - size)), min(cols, int(math.ceil(cx + size)) + 1)
         if y0 >= y1 or x0 >= x1:
             continue
@@ -75,11 +81,16 @@ def make_image(rows: int, cols: int, shapes: int, sigma: float, seed: int = 1,
             yy = np.arange(y0, y1, dtype=np.float32)[:, None] - cy
             xx = np.arange(x0, x1, dtype=np.float32)[None, :] - cx
             m = (yy * yy + xx * xx) <= size * size
-            img[y0:y1, x0:x1][m] = val
+            img[y0 - r0:y1 - r0, x0:x1][m] = val
         else:
-            img[y0:y1, x0:x1] = val
+            img[y0 - r0:y1 - r0, x0:x1] = val
     img += (10.0 * np.sin(2 * np.pi * c / 17.0) * np.cos(2 * np.pi * r / 23.0)).astype(np.float32)
-    img += rng.standard_normal((rows, cols), dtype=np.float32) * np.float32(sigma)
+    # noise: one PCG64 stream per block of NOISE_BLOCK rows (seeded from (seed, block))
+    for b in range(r0 // NOISE_BLOCK, (r1 + NOISE_BLOCK - 1) // NOISE_BLOCK):
+        nrng = np.random.Generator(np.random.PCG64([seed, b]))
+        blk = nrng.standard_normal((NOISE_BLOCK, cols), dtype=np.float32)
+        a, z = max(r0, b * NOISE_BLOCK), min(r1, (b + 1) * NOISE_BLOCK)
+        img[a - r0:z - r0] += blk[a - b * NOISE_BLOCK:z - b * NOISE_BLOCK] * np.float32(sigma)
     if quantize:  # round half away from zero, clamp (quantize_u8, image_io.cpp:54-63)
         img = np.clip(np.sign(img) * np.floor(np.abs(img) + 0.5), 0.0, 255.0).astype(np.float32)
     return img
