@@ -96,6 +96,13 @@ int walk3_lines(int ST) {
   if (forced) return forced;
   return ST <= 10 ? 2 : 1;  // measured on B200: c4 (S=10) 2 lines, c3 (S=15) 1 line
 }
+int walk3_minb() {
+  static const int v = [] {
+    const char* e = std::getenv("PLGPU_MINB");
+    return e ? std::atoi(e) : 1;
+  }();
+  return v;
+}
 // PLGPU_FORCE_WALKER=2 skips only the hot-configuration kernel (walk3).
 bool force_portable_v2() {
   static const bool f = [] {
@@ -211,6 +218,7 @@ int try_pass2(const plgpu::PassDesc& g, cudaStream_t st) {
       d3.b = d;
       // lines per lane for the hot kernel (PLGPU_LINES=1|2 overrides)
       d3.lines = walk3_lines(ST);
+      d3.minb = walk3_minb();
       const int LW3 = 32 * d3.lines;
       d3.b.groups_per_img = (g.lines_per_img + LW3 - 1) / LW3;
       d3.b.total_warps = images * d3.b.groups_per_img * d.nseg;

@@ -83,13 +83,11 @@ bool launch_pass3(const Pass3Desc& d, bool rows, cudaStream_t st) {
     const unsigned blocks = (unsigned)((d.b.total_warps + kWarpsPerCta - 1) / kWarpsPerCta);
     auto go = [&](auto lines_tag) {
       constexpr int L = decltype(lines_tag)::value;
-      if (rows) {
-        const size_t smem = sizeof(float) * kWarpsPerCta * pass3_smem_floats_per_warp<ST, L, true>();
-        nlm_pass3_kernel<ST, KT, L, true><<<blocks, 32 * kWarpsPerCta, smem, st>>>(d);
-      } else {
-        const size_t smem = sizeof(float) * kWarpsPerCta * pass3_smem_floats_per_warp<ST, L, false>();
-        nlm_pass3_kernel<ST, KT, L, false><<<blocks, 32 * kWarpsPerCta, smem, st>>>(d);
-      }
+      const size_t smem_r = sizeof(float) * kWarpsPerCta * pass3_smem_floats_per_warp<ST, L, true>();
+      const size_t smem_c = sizeof(float) * kWarpsPerCta * pass3_smem_floats_per_warp<ST, L, false>();
+      // (register-capped variants, minb 6/8, measured slower on B200: profiles/README.md)
+      if (rows) nlm_pass3_kernel<ST, KT, L, true><<<blocks, 32 * kWarpsPerCta, smem_r, st>>>(d);
+      else nlm_pass3_kernel<ST, KT, L, false><<<blocks, 32 * kWarpsPerCta, smem_c, st>>>(d);
     };
     if constexpr (ST <= 16) {
       if (d.lines == 2) go(std::integral_constant<int, 2>{});

@@ -39,6 +39,7 @@ __host__ __device__ constexpr int pass3_smem_floats_per_warp() {
 struct Pass3Desc {
   Pass2Desc b;          // geometry (strides, lines, segments, coef, S, K)
   int32_t lines;        // lines per lane (1 or 2); b.total_warps / groups follow it
+  int32_t minb;         // register-cap variant (1, 6 or 8)
   int32_t seg_lo, seg_hi;  // interior segment range [seg_lo, seg_hi]
   int64_t interior_warps;  // groups * (seg_hi - seg_lo + 1)
 };
@@ -348,13 +349,10 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
   cp_wait<0>();
 }
 
-// Minimum resident CTAs per SM: caps registers so that three warps fit each
-// SM sub-partition's 16K-register file (<= 168 regs) where the ring state allows.
-template <int ST, int LINES>
-constexpr int pass3_min_blocks() { return 1; }
-
-template <int ST, int KT, int LINES, bool ROWS>
-__global__ void __launch_bounds__(32 * kWarpsPerCta, (pass3_min_blocks<ST, LINES>()))
+// MINB = minimum resident CTAs per SM requested from ptxas: 1 (no cap),
+// 6 (<= 168 registers: 3 warps per SM sub-partition), 8 (<= 128: 4 warps).
+template <int ST, int KT, int LINES, bool ROWS, int MINB = 1>
+__global__ void __launch_bounds__(32 * kWarpsPerCta, MINB)
     nlm_pass3_kernel(const Pass3Desc d) {
   extern __shared__ __align__(16) float smem[];
   const Pass2Desc& g = d.b;

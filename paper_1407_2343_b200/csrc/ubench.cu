@@ -168,12 +168,15 @@ __global__ void pk_kernel(float* out, int iters) {
   constexpr int NC = 8;
   V x[NC], y[NC];
   float xs[NC], ys[NC];
+  int xi[NC], yi[NC];
 #pragma unroll
   for (int k = 0; k < NC; ++k) {
     x[k] = plgpu::f2_make(threadIdx.x * 1e-3f + k, k * 0.5f);
     y[k] = plgpu::f2_make(0.999f - k * 1e-4f, 1.0001f + k * 1e-5f);
     xs[k] = threadIdx.x * 1e-3f + k;
     ys[k] = 0.999f - k * 1e-4f;
+    xi[k] = threadIdx.x * 7 + k;
+    yi[k] = 3 + (int)threadIdx.x * k;
   }
   for (int it = 0; it < iters; ++it) {
 #pragma unroll
@@ -185,9 +188,13 @@ __global__ void pk_kernel(float* out, int iters) {
       if (OP == 3) { x[k] = (k & 1) ? O::add(x[k], y[j]) : O::fma(x[k], y[k], x[j]); }
       if (OP == 4) xs[k] = fmaf(xs[k], ys[k], xs[j]);
       if (OP == 5) xs[k] = xs[k] + ys[j];
+      if (OP == 6) xi[k] = xi[k] * yi[k] + xi[j];
+      if (OP == 7) xi[k] = xi[k] + yi[j] - xi[(k + 5) % NC];
     }
   }
   float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < NC; ++k) s += (float)xi[k];
 #pragma unroll
   for (int k = 0; k < NC; ++k) s += O::lo(x[k]) + O::hi(x[k]) + xs[k];
   if (s == 1.2345f) out[threadIdx.x] = s;
@@ -212,7 +219,9 @@ double plub_pk_rate(int op, int blocks_per_sm, int threads, int iters) {
       case 2: pk_kernel<2><<<blocks, threads>>>(out, iters); break;
       case 3: pk_kernel<3><<<blocks, threads>>>(out, iters); break;
       case 4: pk_kernel<4><<<blocks, threads>>>(out, iters); break;
-      default: pk_kernel<5><<<blocks, threads>>>(out, iters); break;
+      case 5: pk_kernel<5><<<blocks, threads>>>(out, iters); break;
+      case 6: pk_kernel<6><<<blocks, threads>>>(out, iters); break;
+      default: pk_kernel<7><<<blocks, threads>>>(out, iters); break;
     }
   };
   launch();

@@ -397,3 +397,38 @@ def test_slab_transpose_emulated_bitwise():
         colslab = np.concatenate([sends[src][g] for src in range(G)], axis=0)  # recv layout
         got = host(pl.nlm_col_pass(dev(colslab), (S, K, h)))
         assert np.array_equal(got, want[:, g * (W // G):(g + 1) * (W // G)]), g
+
+
+def test_guard_bands_no_stray_access():
+    """Stand-in for compute-sanitizer (closed on this pool): every kernel path runs on
+    inputs/outputs embedded in NaN guard bands.  A stray read poisons an output with
+    NaN; a stray write changes the output guard."""
+    rng = np.random.default_rng(77)
+    G = 4096
+    for (b, r, c) in [(1, 1, 1), (1, 5, 7), (2, 33, 70), (1, 70, 300), (3, 130, 97),
+                      (1, 600, 520), (1, 64, 2048)]:
+        for (S, K) in [(0, 0), (1, 0), (4, 2), (10, 3), (15, 5), (25, 7), (10, 9), (40, 1)]:
+            if K > min(r, c):
+                continue
+            n = b * r * c
+            src = torch.full((n + 2 * G,), float("nan"), device="cuda")
+            dst = torch.full((n + 2 * G,), -7.0, device="cuda")
+            x = src[G:G + n].view(b, r, c)
+            x.copy_(torch.from_numpy(rng.uniform(0, 255, (b, r, c)).astype(np.float32)))
+            y = dst[G:G + n].view(b, r, c)
+            p = (S, K, 60.0)
+            for fn in (pl.nlm_row_pass, pl.nlm_col_pass, pl.snlm_2d_row_col, pl.snlm_2d):
+                fn(x, p, out=y)
+                torch.cuda.synchronize()
+                assert torch.isfinite(y).all(), (b, r, c, S, K, fn.__name__)
+                assert (dst[:G] == -7.0).all() and (dst[G + n:] == -7.0).all(), (b, r, c, S, K)
+            if c % 16 == 0:
+                pl.nlm_row_pass_blocked(x, p, 16, out=y)
+                torch.cuda.synchronize()
+                assert torch.isfinite(y).all()
+                assert (dst[:G] == -7.0).all() and (dst[G + n:] == -7.0).all()
+            line = x[0, 0]
+            out1 = dst[G:G + c]
+            pl.nlm_1d_patchlift(line.contiguous(), p, out=out1)
+            torch.cuda.synchronize()
+            assert torch.isfinite(out1).all() and (dst[:G] == -7.0).all()

@@ -24,7 +24,7 @@ L.plub_pk_rate.restype = C.c_double
 L.plub_pk_rate.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int]
 clk = 1.965e9
 pk = {}
-for op, name in enumerate(["ffma2_3pair", "fadd2_2pair", "fmul2_2pair", "ffma2_fadd2_mix", "ffma_3reg", "fadd_2reg"]):
+for op, name in enumerate(["ffma2_3pair", "fadd2_2pair", "fmul2_2pair", "ffma2_fadd2_mix", "ffma_3reg", "fadd_2reg", "imad_3reg", "iadd3"]):
     for bps, thr in ((4, 128), (8, 128)):
         r = L.plub_pk_rate(op, bps, thr, 4000)
         pk[f"{name}_w{bps*thr//32}"] = {"warp_instr_per_clk_per_sm": r / clk, "cycles_per_instr_per_smsp": 4 * clk / r}
