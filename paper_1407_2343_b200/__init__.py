@@ -21,7 +21,7 @@ from dataclasses import dataclass
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 LIBDIR = os.path.join(PKG, "lib")
-LIBPLGPU = os.path.join(LIBDIR, "libplgpu.so")
+LIBPLGPU = os.environ.get("PLGPU_LIB") or os.path.join(LIBDIR, "libplgpu.so")  # override: experiments
 LIBDROPIN = os.path.join(LIBDIR, "libpatchlift_b200.so")
 
 PL_OK, PL_ERR_VALIDATION, PL_ERR_RANGE, PL_ERR_CUDA, PL_ERR_UNSUPPORTED, PL_ERR_ARG = range(6)

@@ -70,7 +70,14 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 // whole number of S+1-step iterations of the unrolled walker.
 int32_t segment_length(int32_t n, int32_t S) {
   const int32_t R = std::max(1, S + 1);
-  const int32_t C = 256 - (256 + S) % R;
+  static const int32_t target = [] {  // long segments: pre-walk overhead S/C stays small
+    const char* e = std::getenv("PLGPU_SEG");  // experiments only
+    return e ? std::max(16, std::atoi(e)) : 480;
+  }();
+  const int32_t nseg = std::max(1, (n + target - 1) / target);
+  int32_t C = (n + nseg - 1) / nseg;       // near-equal segments
+  C += (R - (C + S) % R) % R;              // C + S: whole S+1-step iterations (round up,
+                                           // so nseg segments still cover the line)
   return n < C ? n : C;
 }
 
@@ -230,7 +237,8 @@ int try_pass2(const plgpu::PassDesc& g, cudaStream_t st) {
         const int s0 = sgi * d.seg_len, s1 = std::min(d.n, s0 + d.seg_len);
         const int i0 = std::max(0, s0 - d.S), T = s1 - i0, pos0 = i0 - 1 - d.K;
         const int nch = (T + R - 1) / R;
-        const bool interior = pos0 >= 0 && pos0 + nch * R + BASE - 1 <= d.n - 1 && T % R == 0;
+        const bool interior = pos0 >= 0 && pos0 + nch * R + BASE - 1 <= d.n - 1 && T % R == 0 &&
+                              s1 - 1 + ST <= d.n - 1;
         if (interior) {
           lo = std::min(lo, sgi);
           hi = std::max(hi, sgi);

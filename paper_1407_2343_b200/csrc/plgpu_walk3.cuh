@@ -17,12 +17,15 @@
 //    -> banks (2u + l) mod 32 are distinct, and the compute reads (LDS.64 of
 //    lines 2l, 2l+1) are contiguous.  Outputs are staged the same way and
 //    leave once per iteration as contiguous row pieces.
-//  * Interior segments (no mirror, no clipped windows) run the EDGE = false
-//    instantiation; the scheduler places all interior warps before the edge
-//    warps so each SM's instruction cache holds one variant at a time.
+//  * One instantiation per configuration: chunks inside the line take the fast
+//    copy path, chunks touching a line end the mirrored one (per chunk, at run
+//    time); every iteration that needs no window clipping runs the branch-free
+//    unmasked body, only the last partial/clipped iteration of a line runs the
+//    masked body (per-step exit, weight 0 for pairs beyond the line end).
 #pragma once
 
 #include <cstdint>
+#include <type_traits>
 
 #include "plgpu_walk2.cuh"
 
@@ -40,11 +43,14 @@ struct Pass3Desc {
   Pass2Desc b;          // geometry (strides, lines, segments, coef, S, K)
   int32_t lines;        // lines per lane (1 or 2); b.total_warps / groups follow it
   int32_t minb;         // register-cap variant (1, 6 or 8)
-  int32_t seg_lo, seg_hi;  // interior segment range [seg_lo, seg_hi]
+  int32_t seg_lo, seg_hi;  // segments whose walk needs no clipping (S > 16 split mode)
   int64_t interior_warps;  // groups * (seg_hi - seg_lo + 1)
 };
 
-template <int ST, int KT, int LINES, bool ROWS, bool EDGE>
+// MODE 0: unified (per-chunk mirror check, per-iteration masked/unmasked
+// body).  MODE 1: interior segment only (no mirrored staging, no masked body
+// compiled: smaller code for large S).  MODE 2: edge segment (always masked).
+template <int ST, int KT, int LINES, bool ROWS, int MODE = 0>
 __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int lane,
                                       const int64_t grp, const int seg) {
   using Ops = VecOps<LINES>;
@@ -62,7 +68,7 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
   const int64_t img = grp / g.groups_per_img;
   const int l0 = (int)(grp % g.groups_per_img) * LW;
   const int n = g.n;
-  const int S = EDGE ? g.S : ST;
+  const int S = g.S;  // effective radius (<= ST; pairs with k > S are masked)
   const int s0 = seg * g.seg_len;
   const int s1 = min(n, s0 + g.seg_len);
   const int i0 = max(0, s0 - S);
@@ -71,66 +77,88 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
   const float* src = g.src + img * g.src_img_stride;
   const int last_line = g.lines_per_img - 1;
   const int nchunks = (T + R - 1) / R;  // body iterations
+  const bool full_group = l0 + LW - 1 <= last_line;
+  // Column pass with 2 lines per lane: every lane stages (8-byte copies) and
+  // flushes exactly the lines it computes -> no warp barriers around the ring.
+  const bool own = !ROWS && LINES == 2 && g.vec16;
 
   auto slot = [&](int c) -> float* { return ring + (c & (kNS3 - 1)) * CHUNK; };
   // Copy chunk c (positions u = cR + BASE + q, q < R); always commits a group.
   // Positions with u < 0 (ahead of the anchor) are never read and not copied.
-  // Addresses advance incrementally (64-bit adds) from per-warp bases.
+  // Chunks entirely inside the line take the fast path (incremental 64-bit
+  // addresses); chunks touching a line end use the half-sample mirror.
   const int lane16 = lane & 15, half = lane >> 4;
   const int64_t ps = g.src_pos_stride, ls = g.src_line_stride;
-  // ROWS: this lane copies lines l0 + 2j + half at positions q = lane16 (+16..)
   const float* rows_base = src + (int64_t)min(l0 + half, last_line) * ls;
   auto issue_chunk = [&](int c) {
     if (c <= nchunks - 1) {
       float* dstc = slot(c);
       const int ubase = c * R + BASE;
+      const int pfirst = pos0 + ubase;
+      const bool inside = MODE == 1 || (MODE == 0 && pfirst >= 0 && pfirst + R - 1 <= n - 1);
       if constexpr (ROWS) {
 #pragma unroll
         for (int qb = 0; qb < R; qb += 16) {
           const int q = qb + lane16;
           if (q < R && ubase + q >= 0) {
-            const int p = pos0 + ubase + q;
+            const int p = pfirst + q;
             float* drow = dstc + q * PITCH + half;
-            if (EDGE || l0 + LW - 1 > last_line) {
-              const float* col = src + (int64_t)(EDGE ? mirror_pos(p, n) : p) * ps;
-#pragma unroll 4
-              for (int j = 0; j < LW / 2; ++j)
-                cp_async4(drow + 2 * j, col + (int64_t)min(l0 + 2 * j + half, last_line) * ls);
-            } else {
+            if (inside && full_group) {
               const float* gp = rows_base + p;
 #pragma unroll 8
               for (int j = 0; j < LW / 2; ++j) {
                 cp_async4(drow + 2 * j, gp);
                 gp += 2 * ls;
               }
+            } else {
+              const float* col = src + (int64_t)mirror_pos(p, n) * ps;
+#pragma unroll 4
+              for (int j = 0; j < LW / 2; ++j)
+                cp_async4(drow + 2 * j, col + (int64_t)min(l0 + 2 * j + half, last_line) * ls);
             }
           }
         }
-      } else if (!EDGE && g.vec16) {
-        if (lane < LW / 4) {
-          const float* gp = src + (int64_t)(pos0 + ubase) * ps + l0 + 4 * lane;
-          float* dp = dstc + 4 * lane;
+      } else if (own) {
+        float* dp = dstc + LINES * lane;
+        if (inside) {
+          const float* gp = src + (int64_t)pfirst * ps + l0 + LINES * lane;
 #pragma unroll
           for (int q = 0; q < R; ++q) {
-            if (ubase + q >= 0) cp_async16(dp, gp);
+            if (ubase + q >= 0) cp_async8(dp, gp);
             gp += ps;
             dp += PITCH;
           }
+        } else {
+#pragma unroll 4
+          for (int q = 0; q < R; ++q) {
+            if (ubase + q >= 0)
+              cp_async8(dp, src + (int64_t)mirror_pos(pfirst + q, n) * ps + l0 + LINES * lane);
+            dp += PITCH;
+          }
+        }
+      } else if (g.vec16) {
+        // one line per lane: 16-byte copies, 32*16/(4*LW) position rows per instruction
+        constexpr int LPR = LW / 4, RPI = 32 / LPR;
+        const int qo = lane / LPR;
+        float* dp = dstc + qo * PITCH + 4 * (lane % LPR);
+#pragma unroll
+        for (int qb = 0; qb < R; qb += RPI) {
+          const int q = qb + qo;
+          if (q < R && ubase + q >= 0) {
+            const int p = inside ? pfirst + q : mirror_pos(pfirst + q, n);
+            cp_async16(dp, src + (int64_t)p * ps + l0 + 4 * (lane % LPR));
+          }
+          dp += RPI * PITCH;
         }
       } else {
 #pragma unroll 4
         for (int q = 0; q < R; ++q) {
           if (ubase + q < 0) continue;
-          const int p = pos0 + ubase + q;
-          const float* rowp = src + (int64_t)(EDGE ? mirror_pos(p, n) : p) * ps;
-          if (g.vec16) {
-            if (lane < LW / 4) cp_async16(dstc + q * PITCH + 4 * lane, rowp + l0 + 4 * lane);
-          } else {
+          const float* rowp = src + (int64_t)mirror_pos(pfirst + q, n) * ps;
 #pragma unroll
-            for (int h = 0; h < LINES; ++h) {
-              const int l = lane * LINES + h;
-              cp_async4(dstc + q * PITCH + l, rowp + (int64_t)min(l0 + l, last_line) * ls);
-            }
+          for (int h = 0; h < LINES; ++h) {
+            const int l = lane * LINES + h;
+            cp_async4(dstc + q * PITCH + l, rowp + (int64_t)min(l0 + l, last_line) * ls);
           }
         }
       }
@@ -196,10 +224,11 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
   const int my_line = l0 + lane * LINES;
 
   for (int c = 0; c < nchunks; ++c) {
-    __syncwarp();       // all lanes done with chunk c-2 (iteration c-1)
-    issue_chunk(c + 2);  // into the slot of chunk c-2
-    cp_wait<2>();       // chunk c landed
-    __syncwarp();
+    // Row pass: lanes read positions staged by other lanes -> warp barriers.
+    if (!own) __syncwarp();  // all lanes done with chunk c-2 (iteration c-1)
+    issue_chunk(c + 2);      // into the slot of chunk c-2
+    cp_wait<2>();            // chunk c landed
+    if (!own) __syncwarp();
     const float* prv = slot(c - 1) + lane * LINES;
     const float* cur = slot(c) + lane * LINES;
     // sample at ring coordinate s + off for body step r (all compile-time but c)
@@ -208,85 +237,114 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
       return q >= 0 ? Ops::lds(cur + q * PITCH) : Ops::lds(prv + (q + R) * PITCH);
     };
     const int sb = c * R;
+    // One iteration = R steps.  MASK = false: all R steps exist and no pair
+    // leaves the line (the common case, branch-free); MASK = true: the last,
+    // partial or clipped iteration(s) -- per-step exit, pairs beyond the line
+    // end (or k > S) get weight exactly 0.
+    auto body = [&](auto mask_tag) {
+      constexpr bool MASK = decltype(mask_tag)::value;
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int s = sb + r;
-      // Interior segments walk a whole number of iterations (the segment
-      // length is chosen so that C + S is a multiple of S+1): no per-step exit,
-      // so the scheduler overlaps consecutive steps.
-      if (EDGE && s >= T) break;
-      const int i = i0 + s;
-      const V an_ = nr[r], ao = orr[r];
-      const int kmax = EDGE ? min(S, n - 1 - i) : ST;
-      V qv;
-      if constexpr (PK) {
-        using O2 = VecOps<2>;
-        const F2 fip = frp[r];
-        F2 nd = O2::add(acc[r], fip);  // {j-side num + f_i, j-side den + 1}
+      for (int r = 0; r < R; ++r) {
+        const int s = sb + r;
+        if (MASK && s >= T) break;
+        const int i = i0 + s;
+        const V an_ = nr[r], ao = orr[r];
+        const int kmax = MASK ? min(S, n - 1 - i) : ST;
+        V qv;
+        if constexpr (PK) {
+          using O2 = VecOps<2>;
+          const F2 fip = frp[r];
+          F2 nd = O2::add(acc[r], fip);  // {j-side num + f_i, j-side den + 1}
 #pragma unroll
-        for (int k = 1; k <= ST; ++k) {
-          const int rk = (r + k) % R;
-          const float dn = an_ - nr[rk];
-          float dk = fmaf(dn, dn, d[k]);
-          const float dq = ao - orr[rk];
-          dk = fmaf(-dq, dq, dk);
-          d[k] = dk;
-          float w = ex2_approx(dk * g.coef);
-          if constexpr (EDGE) w = k > kmax ? 0.f : w;
-          const F2 ww = f2_make(w, w);
-          nd = O2::fma(frp[rk], ww, nd);  // num += w f_{i+k}; den += w
-          // first contribution to the slot recycled at step r-1: fma with 0
-          acc[rk] = O2::fma(fip, ww, k == ST ? zero2 : acc[rk]);
-        }
-        float qn, qd;
-        f2_split(nd, qn, qd);
-        qv = div_fix(qn, qd);
-      } else {
-        const V fi = fr[r];
-        V num = Ops::add(an[r], fi);
-        V den = Ops::add(ad[r], one);
-#pragma unroll
-        for (int k = 1; k <= ST; ++k) {
-          const int rk = (r + k) % R;
-          const V dn = Ops::sub(an_, nr[rk]);
-          V dk = Ops::fma(dn, dn, d[k]);
-          const V dq = Ops::sub(ao, orr[rk]);
-          dk = Ops::fms(dq, dq, dk);
-          d[k] = dk;
-          V w = Ops::ex2(Ops::mul(dk, coefv));
-          if constexpr (EDGE) w = Ops::zero_if(k > kmax, w);
-          num = Ops::fma(w, fr[rk], num);
-          den = Ops::add(w, den);
-          if (k == ST) {  // first contribution to the slot recycled at step r-1
-            an[rk] = Ops::fma(w, fi, zero);  // exactly the portable walker's fma(w, fi, 0)
-            ad[rk] = w;                      // == 0 + w (w >= +0)
-          } else {
-            an[rk] = Ops::fma(w, fi, an[rk]);
-            ad[rk] = Ops::add(w, ad[rk]);
+          for (int k = 1; k <= ST; ++k) {
+            const int rk = (r + k) % R;
+            const float dn = an_ - nr[rk];
+            float dk = fmaf(dn, dn, d[k]);
+            const float dq = ao - orr[rk];
+            dk = fmaf(-dq, dq, dk);
+            d[k] = dk;
+            float w = ex2_approx(dk * g.coef);
+            if constexpr (MASK) w = k > kmax ? 0.f : w;
+            const F2 ww = f2_make(w, w);
+            nd = O2::fma(frp[rk], ww, nd);  // num += w f_{i+k}; den += w
+            // first contribution to the slot recycled at step r-1: fma with 0
+            acc[rk] = O2::fma(fip, ww, k == ST ? zero2 : acc[rk]);
           }
+          float qn, qd;
+          f2_split(nd, qn, qd);
+          qv = div_fix(qn, qd);
+        } else {
+          const V fi = fr[r];
+          V num = Ops::add(an[r], fi);
+          V den = Ops::add(ad[r], one);
+#pragma unroll
+          for (int k = 1; k <= ST; ++k) {
+            const int rk = (r + k) % R;
+            const V dn = Ops::sub(an_, nr[rk]);
+            V dk = Ops::fma(dn, dn, d[k]);
+            const V dq = Ops::sub(ao, orr[rk]);
+            dk = Ops::fms(dq, dq, dk);
+            d[k] = dk;
+            V w = Ops::ex2(Ops::mul(dk, coefv));
+            if constexpr (MASK) w = Ops::zero_if(k > kmax, w);
+            num = Ops::fma(w, fr[rk], num);
+            den = Ops::add(w, den);
+            if (k == ST) {  // first contribution to the slot recycled at step r-1
+              an[rk] = Ops::fma(w, fi, zero);  // exactly the portable walker's fma(w, fi, 0)
+              ad[rk] = w;                      // == 0 + w (w >= +0)
+            } else {
+              an[rk] = Ops::fma(w, fi, an[rk]);
+              ad[rk] = Ops::add(w, ad[rk]);
+            }
+          }
+          qv = Ops::div(num, den);
         }
-        qv = Ops::div(num, den);
+        const float o0 = fminf(fmaxf(Ops::lo(qv), lo0), hi0);
+        float o1 = o0;
+        if constexpr (LINES == 2) o1 = fminf(fmaxf(Ops::hi(qv), lo1), hi1);
+        {  // every step lands in the output ring, filtered at the flush
+          float* sl = oring + r * PITCH + lane * LINES;
+          if constexpr (LINES == 2) *reinterpret_cast<float2*>(sl) = make_float2(o0, o1);
+          else *sl = o0;
+        }
+        // refill slot r in place: first read at step r+1's last offset
+        const V fnew = at(r, 2 + KT + ST);
+        if constexpr (PK) frp[r] = f2_make(Ops::lo(fnew), 1.f);
+        else fr[r] = fnew;
+        nr[r] = at(r, BASE);
+        orr[r] = at(r, 1 + ST);
+        track(fnew);
       }
-      const float o0 = fminf(fmaxf(Ops::lo(qv), lo0), hi0);
-      float o1 = o0;
-      if constexpr (LINES == 2) o1 = fminf(fmaxf(Ops::hi(qv), lo1), hi1);
-      {  // branch-free: every step lands in the output ring, filtered at the flush
-        float* sl = oring + r * PITCH + lane * LINES;
-        if constexpr (LINES == 2) *reinterpret_cast<float2*>(sl) = make_float2(o0, o1);
-        else *sl = o0;
-      }
-      // refill slot r in place: first read at step r+1's last offset
-      const V fnew = at(r, 2 + KT + ST);
-      if constexpr (PK) frp[r] = f2_make(Ops::lo(fnew), 1.f);
-      else fr[r] = fnew;
-      nr[r] = at(r, BASE);
-      orr[r] = at(r, 1 + ST);
-      track(fnew);
+    };
+    if constexpr (MODE == 1) {
+      body(std::integral_constant<bool, false>{});
+    } else if constexpr (MODE == 2) {
+      body(std::integral_constant<bool, true>{});
+    } else {
+      const bool clean = S == ST && sb + R <= T && i0 + sb + R - 1 + ST <= n - 1;
+      if (clean) body(std::integral_constant<bool, false>{});
+      else body(std::integral_constant<bool, true>{});
     }
+
     if constexpr (!ROWS) {
-      // flush this iteration's outputs: row q = position i0 + sb + q, LW lines
-      __syncwarp();
-      if (g.vec16) {
+      // flush this iteration's outputs (row q = position i0 + sb + q)
+      if (own) {  // each lane stores its own lines: no warp barrier
+        float* dp = g.dst + dst_img + (int64_t)(i0 + sb) * g.dst_pos_stride + my_line;
+        const float* sp = oring + LINES * lane;
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+          const int p = i0 + sb + q;
+          if (p >= s0 && p < s1) {
+            if constexpr (LINES == 2)
+              *reinterpret_cast<float2*>(dp) = *reinterpret_cast<const float2*>(sp);
+            else
+              *dp = *sp;
+          }
+          dp += g.dst_pos_stride;
+          sp += PITCH;
+        }
+      } else if (g.vec16) {
+        __syncwarp();
         constexpr int LPR = LW / 4;  // lanes per row, 16 B each
 #pragma unroll
         for (int qb = 0; qb < R; qb += 32 / LPR) {
@@ -298,7 +356,9 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
                                        4 * (lane % LPR)) = v;
           }
         }
+        __syncwarp();
       } else {
+        __syncwarp();
 #pragma unroll 2
         for (int q = 0; q < R; ++q) {
           const int p = i0 + sb + q;
@@ -310,8 +370,8 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
                     oring[q * PITCH + lane * LINES + h];
           }
         }
+        __syncwarp();
       }
-      __syncwarp();
     }
     if constexpr (ROWS) {
       // flush this iteration's outputs: positions p = i0 + sb + q, q < R
@@ -325,7 +385,7 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
           const int64_t pofs =
               (int64_t)(p / blk) * g.dst_block_stride + (int64_t)(p % blk) * g.dst_pos_stride;
           const float* orow = oring + q * PITCH + half;
-          if (l0 + LW - 1 <= last_line) {
+          if (full_group) {
             float* dp = g.dst + dst_img + pofs + (int64_t)(l0 + half) * g.dst_line_stride;
             const int64_t dstep = 2 * g.dst_line_stride;
 #pragma unroll 8
@@ -349,8 +409,6 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
   cp_wait<0>();
 }
 
-// MINB = minimum resident CTAs per SM requested from ptxas: 1 (no cap),
-// 6 (<= 168 registers: 3 warps per SM sub-partition), 8 (<= 128: 4 warps).
 template <int ST, int KT, int LINES, bool ROWS, int MINB = 1>
 __global__ void __launch_bounds__(32 * kWarpsPerCta, MINB)
     nlm_pass3_kernel(const Pass3Desc d) {
@@ -361,15 +419,20 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, MINB)
   const int64_t wid = (int64_t)blockIdx.x * kWarpsPerCta + wib;
   if (wid >= g.total_warps) return;
   float* ring = smem + wib * pass3_smem_floats_per_warp<ST, LINES, ROWS>();
-  const int n_int = max(0, d.seg_hi - d.seg_lo + 1);
-  if (wid < d.interior_warps) {  // interior segments first
-    walk3<ST, KT, LINES, ROWS, false>(g, ring, lane, wid / n_int, d.seg_lo + (int)(wid % n_int));
+  if constexpr (ST <= 16) {
+    walk3<ST, KT, LINES, ROWS, 0>(g, ring, lane, wid / g.nseg, (int)(wid % g.nseg));
   } else {
-    const int n_edge = g.nseg - n_int;
-    const int64_t e = wid - d.interior_warps;
-    int sidx = (int)(e % n_edge);
-    if (n_int > 0 && sidx >= d.seg_lo) sidx += n_int;
-    walk3<ST, KT, LINES, ROWS, true>(g, ring, lane, e / n_edge, sidx);
+    // large S: interior warps (segments needing no clipping) first, then edges
+    const int n_int = max(0, d.seg_hi - d.seg_lo + 1);
+    if (wid < d.interior_warps) {
+      walk3<ST, KT, LINES, ROWS, 1>(g, ring, lane, wid / n_int, d.seg_lo + (int)(wid % n_int));
+    } else {
+      const int n_edge = g.nseg - n_int;
+      const int64_t e = wid - d.interior_warps;
+      int sidx = (int)(e % n_edge);
+      if (n_int > 0 && sidx >= d.seg_lo) sidx += n_int;
+      walk3<ST, KT, LINES, ROWS, 2>(g, ring, lane, e / n_edge, sidx);
+    }
   }
 }
 

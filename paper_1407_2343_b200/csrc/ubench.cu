@@ -72,7 +72,7 @@ __global__ void ffma2_kernel(float* out, int iters, float a, float b) {
 // The walker's per-pair update on register-resident data (no rings, no
 // memory): LINES=2 packed form.  NK independent offsets per step; every
 // accumulation pattern of the real kernel is kept (two num/den chains).
-template <int NK>
+template <int NK, bool PRESCALE = false>
 __global__ void pair2_kernel(float* out, int iters, float c) {
   using O = plgpu::VecOps<2>;
   using V = O::V;
@@ -103,7 +103,7 @@ __global__ void pair2_kernel(float* out, int iters, float c) {
       const V dq = O::sub(b, q[k]);
       dk = O::fms(dq, dq, dk);
       d[k] = dk;
-      const V w = O::ex2(O::mul(dk, cv));
+      const V w = PRESCALE ? O::ex2(dk) : O::ex2(O::mul(dk, cv));
       num = O::fma(w, f[k], num);
       den = O::add(w, den);
       an[k] = O::fma(w, fi, an[k]);
@@ -252,6 +252,7 @@ double plub_pair_rate(int form, int blocks_per_sm, int threads, int iters, doubl
   constexpr int NK = 10;
   auto launch = [&]() {
     if (form == 0) pair2_kernel<NK><<<blocks, threads>>>(out, iters, -1e-4f);
+    else if (form == 2) pair2_kernel<NK, true><<<blocks, threads>>>(out, iters, -1e-4f);
     else pair1_kernel<NK><<<blocks, threads>>>(out, iters, -1e-4f);
   };
   launch();
@@ -268,7 +269,7 @@ double plub_pair_rate(int form, int blocks_per_sm, int threads, int iters, doubl
   cudaEventDestroy(e1);
   cudaFree(out);
   if (cudaGetLastError() != cudaSuccess) return -1;
-  const double pairs = (form == 0 ? 2.0 : 1.0) * NK * (double)iters * blocks * threads * 3;
+  const double pairs = (form != 1 ? 2.0 : 1.0) * NK * (double)iters * blocks * threads * 3;
   if (ms_out) *ms_out = ms / 3;
   return pairs / (ms * 1e-3);
 }

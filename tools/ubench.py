@@ -14,7 +14,7 @@ ms = C.c_double(0)
 res = {}
 for name, w in (("ex2", 0), ("ffma", 1), ("ffma2", 2)):
     res[name + "_per_s"] = L.plub_rate(w, 8, 256, 4096, C.byref(ms))
-for form in (0, 1):
+for form in (0, 1, 2):
     for bps, thr in ((2, 64), (4, 64), (6, 64), (8, 64), (4, 128), (8, 128), (16, 64)):
         r = L.plub_pair_rate(form, bps, thr, 2000, C.byref(ms))
         res[f"pair_form{form}_b{bps}_t{thr}"] = r
