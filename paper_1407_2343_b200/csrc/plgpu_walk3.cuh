@@ -47,6 +47,11 @@ struct Pass3Desc {
   int64_t interior_warps;  // groups * (seg_hi - seg_lo + 1)
 };
 
+// Interior/edge split (two bodies in two instantiations) for radii whose
+// unrolled body is large enough that carrying the masked copy in the same
+// kernel costs instruction-cache hits.
+__host__ __device__ constexpr bool pass3_split(int ST) { return ST > 16; }  // S=15 split measured slower
+
 // MODE 0: unified (per-chunk mirror check, per-iteration masked/unmasked
 // body).  MODE 1: interior segment only (no mirrored staging, no masked body
 // compiled: smaller code for large S).  MODE 2: edge segment (always masked).
@@ -419,7 +424,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, MINB)
   const int64_t wid = (int64_t)blockIdx.x * kWarpsPerCta + wib;
   if (wid >= g.total_warps) return;
   float* ring = smem + wib * pass3_smem_floats_per_warp<ST, LINES, ROWS>();
-  if constexpr (ST <= 16) {
+  if constexpr (!pass3_split(ST)) {
     walk3<ST, KT, LINES, ROWS, 0>(g, ring, lane, wid / g.nseg, (int)(wid % g.nseg));
   } else {
     // large S: interior warps (segments needing no clipping) first, then edges
