@@ -568,35 +568,67 @@ int pl_snlm_2d_row_col_host(const float* host_src, float* host_dst, int32_t batc
   if (!rc) rc = validate_params(p, cols);
   if (!rc) rc = check_ptrs(host_src, host_dst);
   if (rc) return rc;
+  // Three-stage pipeline over images: copy-in (H2D engine), filter (SMs),
+  // copy-out (D2H engine) on three streams ordered by events, NSLOT device
+  // slots of (in, mid, out) so image b+2's upload, image b+1's filter and
+  // image b's download run concurrently.  Group images so each transfer is
+  // >= ~8 MiB (fewer, larger copies).
   cudaStream_t st = as_stream(stream);
   const size_t img = (size_t)rows * cols;
-  // Double-buffered per-image pipeline: H2D(b+1) overlaps compute(b) and D2H(b-1)
-  // through two streams.  Buffers: 2 x (in, mid, out).
+  const int per = (int)std::max<size_t>(1, std::min<size_t>(batch, (8u << 20) / (img * 4) + 1));
+  const int ngroups = (batch + per - 1) / per;
+  constexpr int NSLOT = 3;
+  const size_t slot_elems = 3 * img * per;
   float* buf = nullptr;
-  if ((rc = get_workspace(6 * img * sizeof(float), &buf))) return rc;
-  cudaStream_t s2 = nullptr;
-  PL_CUDA(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
-  cudaStream_t sv[2] = {st, s2};
-  for (int b = 0; b < batch; ++b) {
-    cudaStream_t s = sv[b & 1];
-    float* in = buf + (size_t)(b & 1) * 3 * img;
-    float* mid = in + img;
-    float* out = mid + img;
-    PL_CUDA(cudaMemcpyAsync(in, host_src + (size_t)b * img, img * sizeof(float),
-                            cudaMemcpyHostToDevice, s));
-    if ((rc = run_pass(row_desc(in, mid, 1, rows, cols), p, s))) break;
-    if ((rc = run_pass(col_desc(mid, out, 1, rows, cols), p, s))) break;
-    PL_CUDA(cudaMemcpyAsync(host_dst + (size_t)b * img, out, img * sizeof(float),
-                            cudaMemcpyDeviceToHost, s));
+  if ((rc = get_workspace(NSLOT * slot_elems * sizeof(float), &buf))) return rc;
+  cudaStream_t s_in = nullptr, s_out = nullptr;
+  PL_CUDA(cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking));
+  PL_CUDA(cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking));
+  cudaEvent_t up[NSLOT], done[NSLOT], freed[NSLOT];
+  for (int k = 0; k < NSLOT; ++k) {
+    cudaEventCreateWithFlags(&up[k], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&done[k], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&freed[k], cudaEventDisableTiming);
   }
-  cudaError_t e1 = cudaStreamSynchronize(s2);
-  cudaError_t e2 = cudaStreamSynchronize(st);
-  cudaStreamDestroy(s2);
+  // the caller's stream orders the whole pipeline after prior work
+  cudaEvent_t start;
+  cudaEventCreateWithFlags(&start, cudaEventDisableTiming);
+  cudaEventRecord(start, st);
+  cudaStreamWaitEvent(s_in, start, 0);
+  for (int gi = 0; gi < ngroups && !rc; ++gi) {
+    const int k = gi % NSLOT;
+    const int b0 = gi * per, nb = std::min(per, batch - b0);
+    float* in = buf + k * slot_elems;
+    float* mid = in + img * per;
+    float* out = mid + img * per;
+    if (gi >= NSLOT) cudaStreamWaitEvent(s_in, freed[k], 0);  // slot's previous download done
+    cudaMemcpyAsync(in, host_src + (size_t)b0 * img, nb * img * sizeof(float),
+                    cudaMemcpyHostToDevice, s_in);
+    cudaEventRecord(up[k], s_in);
+    cudaStreamWaitEvent(st, up[k], 0);
+    if ((rc = run_pass(row_desc(in, mid, nb, rows, cols), p, st))) break;
+    if ((rc = run_pass(col_desc(mid, out, nb, rows, cols), p, st))) break;
+    cudaEventRecord(done[k], st);
+    cudaStreamWaitEvent(s_out, done[k], 0);
+    cudaMemcpyAsync(host_dst + (size_t)b0 * img, out, nb * img * sizeof(float),
+                    cudaMemcpyDeviceToHost, s_out);
+    cudaEventRecord(freed[k], s_out);
+  }
+  cudaError_t e1 = cudaStreamSynchronize(s_out);
+  cudaError_t e2 = cudaStreamSynchronize(s_in);
+  cudaError_t e3 = cudaStreamSynchronize(st);
+  for (int k = 0; k < NSLOT; ++k) {
+    cudaEventDestroy(up[k]);
+    cudaEventDestroy(done[k]);
+    cudaEventDestroy(freed[k]);
+  }
+  cudaEventDestroy(start);
+  cudaStreamDestroy(s_in);
+  cudaStreamDestroy(s_out);
   if (rc) return rc;
-  if (e1 != cudaSuccess || e2 != cudaSuccess)
-    return set_err(PL_ERR_CUDA, std::string("host pipeline: ") +
-                                    cudaGetErrorString(e1 != cudaSuccess ? e1 : e2));
-  return PL_OK;
+  const cudaError_t e = e1 != cudaSuccess ? e1 : (e2 != cudaSuccess ? e2 : e3);
+  if (e != cudaSuccess) return set_err(PL_ERR_CUDA, std::string("host pipeline: ") + cudaGetErrorString(e));
+  return check_launch();
 }
 
 
