@@ -112,3 +112,22 @@ def test_product_has_no_oracle_dependency():
     for so in (pl.LIBPLGPU, pl.LIBDROPIN):
         needed = subprocess.run(["readelf", "-d", so], capture_output=True, text=True).stdout
         assert "oracle" not in needed and "patchlift_ref" not in needed
+
+
+def test_bench_reference_arm_runs_on_cpu(tmp_path):
+    """`bench.py --impl reference` needs no GPU: it times the reference library
+    (oracle/_ref) on host cores and prints the contract's JSON line."""
+    import json
+    import sys
+    from oracle import Reference
+    if not Reference.available():
+        pytest.skip("reference library not built")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
+                        "--config", "c2", "--steps", "1", "--warmup", "0"],
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["impl"] == "reference" and line["value"] > 0
+    assert line["unit"] == "Mpixel/s" and line["higher_is_better"] is True
+    assert line["cpu_baseline"]["kind"] == "reference"
+    assert line["e2e"]["h2d_bytes_per_step"] == 0
