@@ -110,6 +110,14 @@ int walk3_minb() {
   }();
   return v;
 }
+int walk3_wpc(int ST) {
+  static const int forced = [] {
+    const char* e = std::getenv("PLGPU_WPC");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (forced == 2 || forced == 8) return forced;
+  return ST >= 15 ? 8 : 2;  // measured: lockstep helps S=15/25 (I-cache), hurts S=10
+}
 // PLGPU_FORCE_WALKER=2 skips only the hot-configuration kernel (walk3).
 bool force_portable_v2() {
   static const bool f = [] {
@@ -226,6 +234,7 @@ int try_pass2(const plgpu::PassDesc& g, cudaStream_t st) {
       // lines per lane for the hot kernel (PLGPU_LINES=1|2 overrides)
       d3.lines = walk3_lines(ST);
       d3.minb = walk3_minb();
+      d3.wpc = walk3_wpc(ST);
       const int LW3 = 32 * d3.lines;
       d3.b.groups_per_img = (g.lines_per_img + LW3 - 1) / LW3;
       d3.b.total_warps = images * d3.b.groups_per_img * d.nseg;

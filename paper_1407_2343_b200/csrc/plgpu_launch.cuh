@@ -86,6 +86,22 @@ bool launch_pass3(const Pass3Desc& d, bool rows, cudaStream_t st) {
       const size_t smem_r = sizeof(float) * kWarpsPerCta * pass3_smem_floats_per_warp<ST, L, true>();
       const size_t smem_c = sizeof(float) * kWarpsPerCta * pass3_smem_floats_per_warp<ST, L, false>();
       // (register-capped variants, minb 6/8, measured slower on B200: profiles/README.md)
+      if (d.wpc == 8) {
+        const int64_t groups = d.b.total_warps / d.b.nseg;
+        const int64_t images = groups / d.b.groups_per_img;
+        const int64_t ctas = images * ((d.b.groups_per_img + 7) / 8) * d.b.nseg;
+        const size_t sr = 4 * smem_r, sc = 4 * smem_c;
+        if (rows) {
+          auto k = nlm_pass3_kernel<ST, KT, L, true, 8>;
+          cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sr);
+          k<<<(unsigned)ctas, 256, sr, st>>>(d);
+        } else {
+          auto k = nlm_pass3_kernel<ST, KT, L, false, 8>;
+          cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sc);
+          k<<<(unsigned)ctas, 256, sc, st>>>(d);
+        }
+        return;
+      }
       if (rows) nlm_pass3_kernel<ST, KT, L, true><<<blocks, 32 * kWarpsPerCta, smem_r, st>>>(d);
       else nlm_pass3_kernel<ST, KT, L, false><<<blocks, 32 * kWarpsPerCta, smem_c, st>>>(d);
     };

@@ -42,7 +42,8 @@ __host__ __device__ constexpr int pass3_smem_floats_per_warp() {
 struct Pass3Desc {
   Pass2Desc b;          // geometry (strides, lines, segments, coef, S, K)
   int32_t lines;        // lines per lane (1 or 2); b.total_warps / groups follow it
-  int32_t minb;         // register-cap variant (1, 6 or 8)
+  int32_t minb;         // unused (register-cap experiments)
+  int32_t wpc;          // warps per CTA: 2 (independent) or 8 (lockstep)
   int32_t seg_lo, seg_hi;  // segments whose walk needs no clipping (S > 16 split mode)
   int64_t interior_warps;  // groups * (seg_hi - seg_lo + 1)
 };
@@ -57,7 +58,7 @@ __host__ __device__ constexpr bool pass3_split(int ST) { return ST > 16; }  // S
 // compiled: smaller code for large S).  MODE 2: edge segment (always masked).
 template <int ST, int KT, int LINES, bool ROWS, int MODE = 0>
 __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int lane,
-                                      const int64_t grp, const int seg) {
+                                      const int64_t grp, const int seg, const int bar_threads = 0) {
   using Ops = VecOps<LINES>;
   using V = typename Ops::V;
   constexpr int LW = 32 * LINES;
@@ -229,6 +230,10 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
   const int my_line = l0 + lane * LINES;
 
   for (int c = 0; c < nchunks; ++c) {
+    // Lockstep CTAs (large S): every warp of the CTA starts each iteration
+    // together, so the SM's warps stream the (large) unrolled body through the
+    // instruction cache once instead of once per warp.
+    if (bar_threads) asm volatile("bar.sync 1, %0;" ::"r"(bar_threads) : "memory");
     // Row pass: lanes read positions staged by other lanes -> warp barriers.
     if (!own) __syncwarp();  // all lanes done with chunk c-2 (iteration c-1)
     issue_chunk(c + 2);      // into the slot of chunk c-2
@@ -414,16 +419,55 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
   cp_wait<0>();
 }
 
-template <int ST, int KT, int LINES, bool ROWS, int MINB = 1>
-__global__ void __launch_bounds__(32 * kWarpsPerCta, MINB)
+// WPC = warps per CTA.  WPC = 2: independent warps.  WPC = 8 ("lockstep"):
+// the CTA's warps take 8 consecutive line groups of ONE segment and
+// synchronise once per iteration (named barrier over the active warps).
+template <int ST, int KT, int LINES, bool ROWS, int WPC = kWarpsPerCta>
+__global__ void __launch_bounds__(32 * WPC, 1)
     nlm_pass3_kernel(const Pass3Desc d) {
   extern __shared__ __align__(16) float smem[];
   const Pass2Desc& g = d.b;
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
-  const int64_t wid = (int64_t)blockIdx.x * kWarpsPerCta + wib;
-  if (wid >= g.total_warps) return;
   float* ring = smem + wib * pass3_smem_floats_per_warp<ST, LINES, ROWS>();
+  if constexpr (WPC == 8) {
+    const int bpi = (g.groups_per_img + 7) / 8;  // 8-group blocks per image
+    const int64_t blocks_per_seg = (g.total_warps / g.nseg + 0) / g.groups_per_img * bpi;
+    const int n_int = pass3_split(ST) ? max(0, d.seg_hi - d.seg_lo + 1) : 0;
+    const int64_t int_ctas = (int64_t)n_int * blocks_per_seg;
+    int seg;
+    int64_t blk;
+    bool interior;
+    if ((int64_t)blockIdx.x < int_ctas) {
+      seg = d.seg_lo + (int)(blockIdx.x % n_int);
+      blk = blockIdx.x / n_int;
+      interior = true;
+    } else {
+      const int64_t e = blockIdx.x - int_ctas;
+      const int n_edge = g.nseg - n_int;
+      int sidx = (int)(e % n_edge);
+      if (n_int > 0 && sidx >= d.seg_lo) sidx += n_int;
+      seg = sidx;
+      blk = e / n_edge;
+      interior = !pass3_split(ST);
+    }
+    const int64_t img = blk / bpi;
+    const int gb = (int)(blk % bpi) * 8;
+    const int active = min(8, g.groups_per_img - gb);
+    if (wib >= active) return;
+    const int64_t grp = img * g.groups_per_img + gb + wib;
+    const int bt = active * 32;
+    if constexpr (!pass3_split(ST)) {
+      walk3<ST, KT, LINES, ROWS, 0>(g, ring, lane, grp, seg, bt);
+    } else if (interior) {
+      walk3<ST, KT, LINES, ROWS, 1>(g, ring, lane, grp, seg, bt);
+    } else {
+      walk3<ST, KT, LINES, ROWS, 2>(g, ring, lane, grp, seg, bt);
+    }
+    return;
+  }
+  const int64_t wid = (int64_t)blockIdx.x * WPC + wib;
+  if (wid >= g.total_warps) return;
   if constexpr (!pass3_split(ST)) {
     walk3<ST, KT, LINES, ROWS, 0>(g, ring, lane, wid / g.nseg, (int)(wid % g.nseg));
   } else {
