@@ -46,6 +46,9 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--c5-dist", default="halo", choices=["halo", "slab"],
+                    help="c5 at N>1: row-partitioned halo exchange (default) or the "
+                         "row-slab -> all-to-all -> column-slab transpose")
     return ap.parse_args()
 
 
@@ -70,9 +73,10 @@ def shard(n_items: int, world: int, rank: int):
     return lo, hi
 
 
-def slab_mode(cfg_name, world):
-    """c5 at N > 1: one image, row slabs -> all-to-all -> column slabs."""
-    return cfg_name == "c5" and world > 1
+def dist_mode(cfg_name, world, how="halo"):
+    """c5 at N > 1 (one image): "halo" (row partition + halo exchange) or
+    "slab" (row slabs -> all-to-all -> column slabs); else None."""
+    return how if cfg_name == "c5" and world > 1 else None
 
 
 def make_inputs(cfg_name, lo, hi, row_range=None):
@@ -278,14 +282,19 @@ def run_ours(args):
     c, S, K, h = workload(args.config)
     params = (S, K, h)
     n_items = c.get("batch", 1)
-    slab = slab_mode(args.config, world)
-    if c["kind"] == "signal" or slab:
+    mode = dist_mode(args.config, world, args.c5_dist)
+    slab, halo = mode == "slab", mode == "halo"
+    if c["kind"] == "signal" or mode:
         lo, hi = 0, 1
     else:
         lo, hi = shard(n_items, world, rank)
     if slab:
         from paper_1407_2343_b200.distributed import SlabPlan
         plan = SlabPlan(c["rows"], c["cols"], world, rank)
+        imgs_host = make_inputs(args.config, 0, 1, row_range=plan.rows)
+    elif halo:
+        from paper_1407_2343_b200.distributed import HaloPlan
+        plan = HaloPlan(c["rows"], c["cols"], world, rank, params)
         imgs_host = make_inputs(args.config, 0, 1, row_range=plan.rows)
     else:
         imgs_host = make_inputs(args.config, lo, hi)
@@ -298,6 +307,19 @@ def run_ours(args):
         cb = c["cols"] // world
         recv = torch.empty_like(x)
         y = torch.empty((c["rows"], cb), dtype=x.dtype, device=dev)
+    if halo:
+        (olo, ohi), (wlo, whi) = plan.rows, plan.window_rows
+        seg_a, seg_b = plan.segments
+        win = torch.empty((whi - wlo, c["cols"]), dtype=x.dtype, device=dev)
+        y = torch.empty((ohi - olo, c["cols"]), dtype=x.dtype, device=dev)
+        p2p = []
+        for s_, d_, lo_, hi_ in plan.transfers():
+            if s_ == rank:
+                p2p.append(torch.distributed.P2POp(torch.distributed.isend,
+                                                   win[lo_ - wlo:hi_ - wlo], d_))
+            elif d_ == rank:
+                p2p.append(torch.distributed.P2POp(torch.distributed.irecv,
+                                                   win[lo_ - wlo:hi_ - wlo], s_))
 
     def first_pass():
         if signal:
@@ -305,6 +327,11 @@ def run_ours(args):
         elif slab:
             pl.nlm_row_pass_blocked(x, params, cb, out=mid)
             torch.distributed.all_to_all_single(recv.reshape(-1), mid.reshape(-1))
+        elif halo:
+            pl.nlm_row_pass(x[0], params, out=win[olo - wlo:ohi - wlo])
+            if p2p:
+                for req in torch.distributed.batch_isend_irecv(p2p):
+                    req.wait()
         else:
             pl.nlm_row_pass(x, params, out=mid)
 
@@ -313,6 +340,8 @@ def run_ours(args):
             return
         if slab:
             pl.nlm_col_pass(recv.reshape(c["rows"], cb), params, out=y)
+        elif halo:
+            pl.nlm_col_pass_window(win, wlo, c["rows"], seg_a, seg_b, params, out=y)
         else:
             pl.nlm_col_pass(mid, params, out=y)
 
@@ -358,8 +387,8 @@ def run_ours(args):
     if signal:
         px_local = c["n"]
         px_total = px_local
-    elif slab:
-        px_local = c["rows"] * c["cols"] // world
+    elif mode:
+        px_local = x.numel() if halo else c["rows"] * c["cols"] // world
         px_total = c["rows"] * c["cols"]
     else:
         px_local = (hi - lo) * c["rows"] * c["cols"]
@@ -373,6 +402,9 @@ def run_ours(args):
     elif slab:
         u_row = (c["rows"] // world) * pl.unique_pairs(c["cols"], S)
         u_col = (c["cols"] // world) * pl.unique_pairs(c["rows"], S)
+    elif halo:  # pairs counted at their left endpoint, which my rows own
+        u_row = (ohi - olo) * pl.unique_pairs(c["cols"], S)
+        u_col = c["cols"] * sum(min(S, c["rows"] - 1 - i) for i in range(olo, ohi))
     else:
         u_row = (hi - lo) * c["rows"] * pl.unique_pairs(c["cols"], S)
         u_col = (hi - lo) * c["cols"] * pl.unique_pairs(c["rows"], S)
@@ -428,9 +460,9 @@ def run_ours(args):
         }
 
     # ---- e2e through the C-ABI host entry point (N GPUs: each rank its shard) --
-    if slab:
+    if mode:
         hin = torch.from_numpy(imgs_host).pin_memory()
-        hout = torch.empty((c["rows"], cb), dtype=torch.float32).pin_memory()
+        hout = torch.empty(tuple(y.shape), dtype=torch.float32).pin_memory()
         torch.cuda.synchronize()
         torch.distributed.barrier()
         t0 = time.perf_counter()
@@ -445,10 +477,17 @@ def run_ours(args):
         if rank == 0:
             line["e2e"] = {"value": px_total / float(te.item()) / 1e6, "unit": UNIT,
                            "h2d_bytes_per_step": int(hin.numel() * 4) * world,
-                           "d2h_bytes_per_step": int(hout.numel() * 4) * world,
-                           "api": "pinned H2D + row pass + NCCL all-to-all + column pass + D2H"}
-            line["config"]["nvlink_bytes_per_rank"] = plan.nvlink_bytes()
-            line["config"]["parallelism"] = f"row slabs -> all-to-all -> column slabs x{world}"
+                           "d2h_bytes_per_step": int(hout.numel() * 4) * world}
+            if slab:
+                line["e2e"]["api"] = "pinned H2D + row pass + NCCL all-to-all + column pass + D2H"
+                line["config"]["nvlink_bytes_per_rank"] = plan.nvlink_bytes()
+                line["config"]["parallelism"] = f"row slabs -> all-to-all -> column slabs x{world}"
+            else:
+                line["e2e"]["api"] = ("pinned H2D + row pass + NCCL halo send/recv + windowed "
+                                      "column pass + D2H")
+                line["config"]["nvlink_bytes_per_rank"] = plan.halo_bytes()
+                line["config"]["parallelism"] = (f"row partition (whole column segments) + "
+                                                 f"halo exchange x{world}")
     elif not signal:
         hin = torch.from_numpy(imgs_host).pin_memory()
         hout = torch.empty_like(hin).pin_memory()

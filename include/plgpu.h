@@ -8,6 +8,7 @@
  *   pl_nlm_lines           nlm_1d_patchlift            nlm.hpp:30, nlm.cpp:144-166
  *   pl_nlm_row_pass        nlm_row_pass                nlm.hpp:39-40, nlm.cpp:215-227
  *   pl_nlm_col_pass        nlm_col_pass                nlm.hpp:41-42, nlm.cpp:229-232
+ *   pl_nlm_col_pass_window nlm_col_pass on a row window (multi-GPU halo form of the same)
  *   pl_snlm_2d_row_col     snlm_2d_row_col             nlm.hpp:45-46, nlm.cpp:234-239
  *   pl_snlm_2d_col_row     snlm_2d_col_row             nlm.hpp:47-48, nlm.cpp:241-246
  *   pl_snlm_2d             snlm_2d (RC+CR)/2           nlm.hpp:51-52, nlm.cpp:248-253
@@ -106,6 +107,23 @@ int pl_nlm_row_pass(const float* src, float* dst, int32_t batch, int32_t rows, i
                     pl_params p, void* stream);
 int pl_nlm_col_pass(const float* src, float* dst, int32_t batch, int32_t rows, int32_t cols,
                     pl_params p, void* stream);
+
+/* Windowed column pass (row-partitioned multi-GPU, halo exchange; SURVEY.md
+ * sec. 8(f)).  The column pass of an image with rows_total rows is cut into
+ * segments of pl_segment_length(rows_total, min(S, rows_total-1)) rows; this
+ * produces segments [seg_begin, seg_end), i.e. output rows [out_lo, out_hi),
+ * bit-identical to the same rows of pl_nlm_col_pass on the whole image.
+ *   pl_col_window: the input rows [in_lo, in_hi) the pass may read for that
+ *     segment range (walker over-fetch included) and the output rows.
+ *   pl_nlm_col_pass_window: src holds input rows [in_lo, in_lo + in_rows)
+ *     (must cover pl_col_window's range), per image [in_rows][cols];
+ *     dst holds output rows [out_lo, out_hi), per image [out_hi-out_lo][cols].
+ *     Needs 1 <= min(S, rows_total-1) <= 32. */
+int pl_col_window(int32_t rows_total, int32_t seg_begin, int32_t seg_end, pl_params p,
+                  int32_t* in_lo, int32_t* in_hi, int32_t* out_lo, int32_t* out_hi);
+int pl_nlm_col_pass_window(const float* src, int32_t in_lo, int32_t in_rows, float* dst,
+                           int32_t batch, int32_t rows_total, int32_t cols, int32_t seg_begin,
+                           int32_t seg_end, pl_params p, void* stream);
 
 /* Row pass whose output is written in column blocks of width col_block:
  * element (b, r, c) lands at dst + b*rows*cols + (c / col_block)*rows*col_block

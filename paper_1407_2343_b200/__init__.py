@@ -35,6 +35,7 @@ EXPORTS = [
     "pl_snlm_2d_col_row", "pl_snlm_2d", "pl_snlm_2d_row_col_host", "pl_nlm_2d_naive",
     "pl_device_alloc", "pl_device_free", "pl_copy_to_device", "pl_copy_to_host",
     "pl_synchronize", "pl_distance_band_f32", "pl_distance_band_i32", "pl_banded_kernel_f64",
+    "pl_col_window", "pl_nlm_col_pass_window",
 ]
 
 
@@ -93,6 +94,9 @@ def lib() -> C.CDLL:
             "pl_nlm_row_pass": ([vp, vp, i32, i32, i32, P, vp], C.c_int),
             "pl_nlm_col_pass": ([vp, vp, i32, i32, i32, P, vp], C.c_int),
             "pl_nlm_row_pass_blocked": ([vp, vp, i32, i32, i32, i32, P, vp], C.c_int),
+            "pl_col_window": ([i32, i32, i32, P] + [C.POINTER(i32)] * 4, C.c_int),
+            "pl_nlm_col_pass_window": ([vp, i32, i32, vp, i32, i32, i32, i32, i32, P, vp],
+                                       C.c_int),
             "pl_workspace_bytes": ([i32, i32, i32, i32], C.c_size_t),
             "pl_snlm_2d_row_col": ([vp, vp, vp, i32, i32, i32, P, vp], C.c_int),
             "pl_snlm_2d_col_row": ([vp, vp, vp, i32, i32, i32, P, vp], C.c_int),
@@ -254,6 +258,38 @@ def nlm_row_pass_blocked(x, p, col_block: int, out=None):
     out = torch.empty_like(x) if out is None else out
     _check(lib().pl_nlm_row_pass_blocked(x.data_ptr(), out.data_ptr(), b, r, c, int(col_block),
                                          _params(p), _stream(x)))
+    return out
+
+
+def col_window(rows_total: int, seg_begin: int, seg_end: int, p):
+    """(in_lo, in_hi, out_lo, out_hi): input rows the windowed column pass over
+    segments [seg_begin, seg_end) reads, and the output rows it produces."""
+    v = [C.c_int32() for _ in range(4)]
+    _check(lib().pl_col_window(int(rows_total), int(seg_begin), int(seg_end), _params(p),
+                               *[C.byref(x) for x in v]))
+    return tuple(x.value for x in v)
+
+
+def col_segments(rows_total: int, p) -> int:
+    """Number of column-pass segments of a rows_total-row image."""
+    S = min(int(_params(p).search_radius), rows_total - 1)
+    C_ = segment_length(rows_total, S)
+    return (rows_total + C_ - 1) // C_
+
+
+def nlm_col_pass_window(x_win, in_lo: int, rows_total: int, seg_begin: int, seg_end: int, p,
+                        out=None):
+    """Column pass of segments [seg_begin, seg_end) from input rows
+    [in_lo, in_lo + x_win.shape[-2]); returns rows [out_lo, out_hi)."""
+    import torch
+    _dev(x_win, torch.float32)
+    b, r, c = _image_dims(x_win)
+    _, _, out_lo, out_hi = col_window(rows_total, seg_begin, seg_end, p)
+    shape = (out_hi - out_lo, c) if x_win.dim() == 2 else (b, out_hi - out_lo, c)
+    out = torch.empty(shape, dtype=torch.float32, device=x_win.device) if out is None else out
+    _check(lib().pl_nlm_col_pass_window(x_win.data_ptr(), int(in_lo), r, out.data_ptr(), b,
+                                        int(rows_total), c, int(seg_begin), int(seg_end),
+                                        _params(p), _stream(x_win)))
     return out
 
 

@@ -63,18 +63,21 @@ int validate_image(int batch, int rows, int cols) {
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
-// Segment length: a function of the line length (and S) only.
 // Segment length: a function of (n, S) only, identical for rows and columns
-// (transpose equivariance) and for every launch shape.  About 256 samples,
-// trimmed so that an interior segment's walk (C + S steps, S of pre-walk) is a
-// whole number of S+1-step iterations of the unrolled walker.
+// (transpose equivariance) and for every launch shape or GPU count.  About
+// 480 samples, rounded up so that an interior segment's walk (C + S steps, S
+// of pre-walk) is a whole number of S+1-step iterations of the unrolled
+// walker.  Lines of 8192+ samples use a multiple of 8 segments, so that the
+// row-partitioned multi-GPU column pass (whole segments per rank) splits
+// evenly over 2, 4 or 8 GPUs.
 int32_t segment_length(int32_t n, int32_t S) {
   const int32_t R = std::max(1, S + 1);
   static const int32_t target = [] {  // long segments: pre-walk overhead S/C stays small
     const char* e = std::getenv("PLGPU_SEG");  // experiments only
     return e ? std::max(16, std::atoi(e)) : 480;
   }();
-  const int32_t nseg = std::max(1, (n + target - 1) / target);
+  int32_t nseg = std::max(1, (n + target - 1) / target);
+  if (n >= 8192) nseg = std::max(8, (nseg + 4) / 8 * 8);
   int32_t C = (n + nseg - 1) / nseg;       // near-equal segments
   C += (R - (C + S) % R) % R;              // C + S: whole S+1-step iterations (round up,
                                            // so nseg segments still cover the line)
@@ -215,6 +218,7 @@ int try_pass2(const plgpu::PassDesc& g, cudaStream_t st) {
   d.n = g.n;
   d.seg_len = g.seg_len;
   d.nseg = g.nseg;
+  d.seg_begin = g.seg_begin;
   d.S = g.S;
   d.K = g.K;
   d.coef = g.coef;
@@ -243,7 +247,7 @@ int try_pass2(const plgpu::PassDesc& g, cudaStream_t st) {
                    g.dst_img_stride % 4 == 0 && a16(g.src) && a16(g.dst);
       int lo = d.nseg, hi = -1;
       for (int sgi = 0; sgi < d.nseg; ++sgi) {
-        const int s0 = sgi * d.seg_len, s1 = std::min(d.n, s0 + d.seg_len);
+        const int s0 = (d.seg_begin + sgi) * d.seg_len, s1 = std::min(d.n, s0 + d.seg_len);
         const int i0 = std::max(0, s0 - d.S), T = s1 - i0, pos0 = i0 - 1 - d.K;
         const int nch = (T + R - 1) / R;
         const bool interior = pos0 >= 0 && pos0 + nch * R + BASE - 1 <= d.n - 1 && T % R == 0 &&
@@ -287,7 +291,10 @@ int run_pass(plgpu::PassDesc g, const pl_params& p, cudaStream_t st) {
   g.K = p.patch_radius;
   g.coef = weight_coef(p.h);
   g.seg_len = segment_length(g.n, g.S);
-  g.nseg = (g.n + g.seg_len - 1) / g.seg_len;
+  if (g.nseg <= 0) {  // whole lines (windowed passes preset seg_begin / nseg)
+    g.seg_begin = 0;
+    g.nseg = (g.n + g.seg_len - 1) / g.seg_len;
+  }
   if (g.dst_pos_block <= 0) g.dst_pos_block = g.n;
   if (g.n_lines <= 0) return PL_OK;
   if (g.n_lines % g.lines_per_img == 0) {
@@ -503,6 +510,79 @@ int pl_nlm_col_pass(const float* src, float* dst, int32_t batch, int32_t rows, i
   if (!rc) rc = check_ptrs(src, dst);
   if (rc) return rc;
   return run_pass(col_desc(src, dst, batch, rows, cols), p, as_stream(stream));
+}
+
+// Rows of the column-pass input that the walkers may read (loads, staging
+// over-fetch included) while producing segments [seg_begin, seg_end): the
+// exact recurrence needs [s0 - S - K - 1, s1 + 2S + K] (walk3 chunk ring);
+// the chunked v2 walker stages up to 16 rows ahead of its anchor and
+// 2K + 80 rows past the last window.  Positions past a line end are
+// half-sample mirrored, exactly as the kernels do.
+static void col_window(int32_t n, int32_t S, int32_t K, int32_t seg_begin, int32_t seg_end,
+                       int32_t* in_lo, int32_t* in_hi, int32_t* out_lo, int32_t* out_hi) {
+  const int32_t C = segment_length(n, S);
+  const int32_t s0 = seg_begin * C, s1 = std::min(n, seg_end * C);
+  const int64_t lo_raw = (int64_t)s0 - S - K - 1 - 16;
+  const int64_t hi_raw = (int64_t)s1 + 2 * S + 2 * K + 81;  // exclusive
+  auto mirror = [n](int64_t p) -> int32_t {
+    p = p < 0 ? -1 - p : p;
+    p = p >= n ? 2 * (int64_t)n - 1 - p : p;
+    return (int32_t)std::min<int64_t>(std::max<int64_t>(p, 0), n - 1);
+  };
+  int32_t lo = (int32_t)std::max<int64_t>(0, std::min<int64_t>(lo_raw, n - 1));
+  int32_t hi = (int32_t)std::min<int64_t>(n, std::max<int64_t>(hi_raw, 1));
+  // Mirrored reads land within S+K+17 rows of a line end; widen to cover them.
+  if (lo_raw < 0) hi = std::max(hi, mirror(lo_raw) + 1);
+  if (hi_raw > n) lo = std::min(lo, mirror(hi_raw - 1));
+  *in_lo = lo;
+  *in_hi = hi;
+  *out_lo = s0;
+  *out_hi = s1;
+}
+
+int pl_col_window(int32_t rows_total, int32_t seg_begin, int32_t seg_end, pl_params p,
+                  int32_t* in_lo, int32_t* in_hi, int32_t* out_lo, int32_t* out_hi) {
+  int rc = validate_params(p, rows_total);
+  if (rc) return rc;
+  if (!in_lo || !in_hi || !out_lo || !out_hi) return set_err(PL_ERR_ARG, "null output pointer");
+  const int32_t S = std::min<int32_t>(p.search_radius, rows_total - 1);
+  const int32_t C = segment_length(rows_total, S);
+  const int32_t nseg = (rows_total + C - 1) / C;
+  if (seg_begin < 0 || seg_end > nseg || seg_begin >= seg_end)
+    return set_err(PL_ERR_RANGE, "segment range out of range");
+  col_window(rows_total, S, p.patch_radius, seg_begin, seg_end, in_lo, in_hi, out_lo, out_hi);
+  return PL_OK;
+}
+
+int pl_nlm_col_pass_window(const float* src, int32_t in_lo, int32_t in_rows, float* dst,
+                           int32_t batch, int32_t rows_total, int32_t cols, int32_t seg_begin,
+                           int32_t seg_end, pl_params p, void* stream) {
+  int rc = validate_image(batch, rows_total, cols);
+  if (!rc) rc = validate_params(p, rows_total);
+  if (!rc) rc = check_ptrs(src, dst);
+  if (rc) return rc;
+  int32_t need_lo, need_hi, out_lo, out_hi;
+  if ((rc = pl_col_window(rows_total, seg_begin, seg_end, p, &need_lo, &need_hi, &out_lo,
+                          &out_hi)))
+    return rc;
+  if (in_lo < 0 || in_rows < 1 || in_lo > need_lo || (int64_t)in_lo + in_rows < need_hi ||
+      (int64_t)in_lo + in_rows > rows_total)
+    return set_err(PL_ERR_RANGE, "input window does not cover the rows pl_col_window requires");
+  const int32_t S = std::min<int32_t>(p.search_radius, rows_total - 1);
+  if (S < 1 || S > kMaxWalkS)
+    return set_err(PL_ERR_UNSUPPORTED, "windowed column pass needs 1 <= S <= 32");
+  // Global row coordinates: the kernels address src/dst as if they held the
+  // whole line (only rows inside the windows are ever touched).
+  plgpu::PassDesc g = col_desc(nullptr, nullptr, batch, rows_total, cols);
+  g.src = reinterpret_cast<const float*>(reinterpret_cast<uintptr_t>(src) -
+                                         (uintptr_t)in_lo * cols * sizeof(float));
+  g.dst = reinterpret_cast<float*>(reinterpret_cast<uintptr_t>(dst) -
+                                   (uintptr_t)out_lo * cols * sizeof(float));
+  g.src_img_stride = (int64_t)in_rows * cols;
+  g.dst_img_stride = (int64_t)(out_hi - out_lo) * cols;
+  g.seg_begin = seg_begin;
+  g.nseg = seg_end - seg_begin;
+  return run_pass(g, p, as_stream(stream));
 }
 
 int pl_nlm_row_pass_blocked(const float* src, float* dst, int32_t batch, int32_t rows,

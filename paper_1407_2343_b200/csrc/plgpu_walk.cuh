@@ -53,7 +53,8 @@ struct PassDesc {
   int32_t lines_per_img;
   int32_t n;        // line length
   int32_t seg_len;  // C
-  int32_t nseg;     // ceil(n / C)
+  int32_t nseg;     // segments processed (ceil(n / C) unless windowed)
+  int32_t seg_begin;  // index of the first processed segment (windowed passes)
   int32_t S;        // effective search radius, <= template S, <= n-1
   int32_t K;        // patch radius
   float coef;       // -log2(e) / h^2
@@ -192,7 +193,7 @@ __global__ void __launch_bounds__(128) nlm_pass_kernel(PassDesc g) {
   const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (w >= g.n_lines * g.nseg) return;
   const int64_t line = w % g.n_lines;
-  const int seg = (int)(w / g.n_lines);
+  const int seg = g.seg_begin + (int)(w / g.n_lines);
   const int64_t img = line / g.lines_per_img;
   const int64_t li = line - img * g.lines_per_img;
   const float* src = g.src + img * g.src_img_stride + li * g.src_line_stride;

@@ -163,6 +163,7 @@ struct Pass2Desc {
   int32_t lines_per_img;
   int32_t groups_per_img;
   int32_t n, seg_len, nseg, S, K;
+  int32_t seg_begin;  // first processed segment (windowed passes; nseg counts from it)
   int32_t vec16;  // column pass: 16-byte copies legal (aligned, full line groups)
   int64_t total_warps;
   float coef;
@@ -215,7 +216,7 @@ __device__ __forceinline__ void walk2(const Pass2Desc& g, float* ring, const int
   constexpr int NRING = ONE ? P : R;
   float* oring = ring + kSR * LW;
 
-  const int seg = (int)(wid % g.nseg);
+  const int seg = g.seg_begin + (int)(wid % g.nseg);
   const int64_t grp = wid / g.nseg;
   const int64_t img = grp / g.groups_per_img;
   const int l0 = (int)(grp % g.groups_per_img) * LW;
@@ -448,7 +449,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) nlm_pass2_kernel(const Pass
   float* ring = smem + wib * pass2_smem_floats_per_warp<LINES, ROWS>();
   // Interior segments (the bulk) need neither mirrored staging nor pair
   // masking: everything the warp ever stages lies inside the line.
-  const int seg = (int)(wid % g.nseg);
+  const int seg = g.seg_begin + (int)(wid % g.nseg);
   const int s0 = seg * g.seg_len;
   const int s1 = min(g.n, s0 + g.seg_len);
   const int K = KT >= 0 ? KT : g.K;

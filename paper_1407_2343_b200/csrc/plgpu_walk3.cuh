@@ -44,7 +44,7 @@ struct Pass3Desc {
   int32_t lines;        // lines per lane (1 or 2); b.total_warps / groups follow it
   int32_t minb;         // unused (register-cap experiments)
   int32_t wpc;          // warps per CTA: 2 (independent) or 8 (lockstep)
-  int32_t seg_lo, seg_hi;  // segments whose walk needs no clipping (S > 16 split mode)
+  int32_t seg_lo, seg_hi;  // segments (relative to b.seg_begin) needing no clipping (S > 16)
   int64_t interior_warps;  // groups * (seg_hi - seg_lo + 1)
 };
 
@@ -439,7 +439,7 @@ __global__ void __launch_bounds__(32 * WPC, 1)
     int64_t blk;
     bool interior;
     if ((int64_t)blockIdx.x < int_ctas) {
-      seg = d.seg_lo + (int)(blockIdx.x % n_int);
+      seg = g.seg_begin + d.seg_lo + (int)(blockIdx.x % n_int);
       blk = blockIdx.x / n_int;
       interior = true;
     } else {
@@ -447,7 +447,7 @@ __global__ void __launch_bounds__(32 * WPC, 1)
       const int n_edge = g.nseg - n_int;
       int sidx = (int)(e % n_edge);
       if (n_int > 0 && sidx >= d.seg_lo) sidx += n_int;
-      seg = sidx;
+      seg = g.seg_begin + sidx;
       blk = e / n_edge;
       interior = !pass3_split(ST);
     }
@@ -469,18 +469,19 @@ __global__ void __launch_bounds__(32 * WPC, 1)
   const int64_t wid = (int64_t)blockIdx.x * WPC + wib;
   if (wid >= g.total_warps) return;
   if constexpr (!pass3_split(ST)) {
-    walk3<ST, KT, LINES, ROWS, 0>(g, ring, lane, wid / g.nseg, (int)(wid % g.nseg));
+    walk3<ST, KT, LINES, ROWS, 0>(g, ring, lane, wid / g.nseg, g.seg_begin + (int)(wid % g.nseg));
   } else {
     // large S: interior warps (segments needing no clipping) first, then edges
     const int n_int = max(0, d.seg_hi - d.seg_lo + 1);
     if (wid < d.interior_warps) {
-      walk3<ST, KT, LINES, ROWS, 1>(g, ring, lane, wid / n_int, d.seg_lo + (int)(wid % n_int));
+      walk3<ST, KT, LINES, ROWS, 1>(g, ring, lane, wid / n_int,
+                                     g.seg_begin + d.seg_lo + (int)(wid % n_int));
     } else {
       const int n_edge = g.nseg - n_int;
       const int64_t e = wid - d.interior_warps;
       int sidx = (int)(e % n_edge);
       if (n_int > 0 && sidx >= d.seg_lo) sidx += n_int;
-      walk3<ST, KT, LINES, ROWS, 2>(g, ring, lane, e / n_edge, sidx);
+      walk3<ST, KT, LINES, ROWS, 2>(g, ring, lane, e / n_edge, g.seg_begin + sidx);
     }
   }
 }

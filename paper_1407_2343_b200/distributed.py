@@ -16,6 +16,16 @@ line length):
   [H][W/G] column slab, which the column pass consumes in place.  Output stays
   as column slabs.
 
+* **Halo exchange** (config c5, the alternative of SURVEY.md sec. 8(f)):
+  ranks own contiguous runs of whole column-pass segments, i.e. contiguous
+  row ranges.  Rank g runs the row pass on its own rows straight into a
+  window buffer covering the rows its column segments read
+  (``pl_col_window``), receives the missing rows (a few dozen above and a
+  few hundred below, from the neighbours that own them) by point-to-point
+  sends, and runs the windowed column pass (``pl_nlm_col_pass_window``).
+  Output stays as row slabs; NVLink traffic per rank is the halo only
+  (~13 MB for c5 on 8 GPUs, against 117 MB for the all-to-all).
+
 The pass and exchange callables are injectable so the host logic (slab plan,
 layouts, exchange) is tested on CPU with gloo and the oracle's passes
 (tests/test_distributed.py).
@@ -95,3 +105,113 @@ def blocked_layout(x, col_block: int):
     element (r, c) -> block c // cb, [r][c % cb] within the block."""
     rows, cols = x.shape[-2], x.shape[-1]
     return x.reshape(rows, cols // col_block, col_block).transpose(1, 0, 2).copy()
+
+
+@dataclass
+class HaloPlan:
+    """Row-partitioned plan for one H x W image over G ranks: rank q owns the
+    column-pass segments [seg[q], seg[q+1]) (whole segments, so the column
+    pass is bitwise the single-GPU one) and the rows they produce.
+
+    ``window(H, seg_begin, seg_end, params) -> (in_lo, in_hi, out_lo, out_hi)``
+    defaults to the library's ``pl_col_window``."""
+
+    H: int
+    W: int
+    world: int
+    rank: int
+    params: tuple
+    window: Callable | None = None
+
+    def __post_init__(self):
+        if self.world < 1 or not 0 <= self.rank < self.world:
+            raise ValueError("bad world/rank")
+        import paper_1407_2343_b200 as pl
+        win = self.window or pl.col_window
+        self.nseg = pl.col_segments(self.H, self.params)
+        self.seg = [self.nseg * q // self.world for q in range(self.world + 1)]
+        self.own, self.need = [], []
+        for q in range(self.world):
+            a, b = self.seg[q], self.seg[q + 1]
+            if b > a:
+                in_lo, in_hi, out_lo, out_hi = win(self.H, a, b, self.params)
+            else:  # more ranks than segments: nothing to do
+                in_lo = in_hi = out_lo = out_hi = 0
+            self.own.append((out_lo, out_hi))
+            self.need.append((in_lo, in_hi))
+
+    @property
+    def segments(self) -> tuple[int, int]:
+        return self.seg[self.rank], self.seg[self.rank + 1]
+
+    @property
+    def rows(self) -> tuple[int, int]:  # rows this rank owns (input and output)
+        return self.own[self.rank]
+
+    @property
+    def window_rows(self) -> tuple[int, int]:  # rows of the column-pass input window
+        return self.need[self.rank]
+
+    def transfers(self) -> list[tuple[int, int, int, int]]:
+        """Every (src_rank, dst_rank, lo, hi): rows [lo, hi) of src's row-pass
+        output that dst's window needs."""
+        out = []
+        for d in range(self.world):
+            nlo, nhi = self.need[d]
+            for s in range(self.world):
+                olo, ohi = self.own[s]
+                lo, hi = max(nlo, olo), min(nhi, ohi)
+                if s != d and hi > lo:
+                    out.append((s, d, lo, hi))
+        return out
+
+    def halo_bytes(self, itemsize: int = 4) -> int:
+        """Bytes this rank receives over NVLink."""
+        return sum((hi - lo) * self.W * itemsize for s, d, lo, hi in self.transfers()
+                   if d == self.rank)
+
+
+def halo_rc(x_rows, params, plan: HaloPlan, *, row_pass: Callable | None = None,
+            col_pass_window: Callable | None = None, exchange: Callable | None = None,
+            new_buffer: Callable | None = None):
+    """Row pass on my rows -> halo exchange -> windowed column pass.
+
+    x_rows: [out_hi - out_lo, W], my rows ``plan.rows`` of the image.  Returns
+    the same rows of snlm_2d_row_col(image).  ``exchange(ops)`` gets a list of
+    ("send"|"recv", peer, tensor) and must complete them all (default:
+    ``torch.distributed.batch_isend_irecv``)."""
+    import torch
+    if row_pass is None:
+        import paper_1407_2343_b200 as pl
+        row_pass = lambda x, p, out: pl.nlm_row_pass(x, p, out=out)  # noqa: E731
+        col_pass_window = col_pass_window or (
+            lambda y, in_lo, H, a, b, p: pl.nlm_col_pass_window(y, in_lo, H, a, b, p))
+    if exchange is None:
+        exchange = _p2p_exchange
+    olo, ohi = plan.rows
+    wlo, whi = plan.window_rows
+    if ohi <= olo:
+        return x_rows[:0]
+    if new_buffer is None:
+        new_buffer = lambda shape: torch.empty(shape, dtype=x_rows.dtype,  # noqa: E731
+                                               device=x_rows.device)
+    y = new_buffer((whi - wlo, plan.W))
+    row_pass(x_rows, params, y[olo - wlo:ohi - wlo])
+    ops = []
+    for s, d, lo, hi in plan.transfers():
+        if s == plan.rank:
+            ops.append(("send", d, y[lo - wlo:hi - wlo]))
+        elif d == plan.rank:
+            ops.append(("recv", s, y[lo - wlo:hi - wlo]))
+    if ops:
+        exchange(ops)
+    a, b = plan.segments
+    return col_pass_window(y, wlo, plan.H, a, b, params)
+
+
+def _p2p_exchange(ops):
+    import torch.distributed as dist
+    p2p = [dist.P2POp(dist.isend if kind == "send" else dist.irecv, t, peer)
+           for kind, peer, t in ops]
+    for req in dist.batch_isend_irecv(p2p):
+        req.wait()

@@ -13,7 +13,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_1407_2343_b200.distributed import SlabPlan, blocked_layout, shard, slab_rc
+from paper_1407_2343_b200.distributed import (HaloPlan, SlabPlan, blocked_layout, halo_rc, shard,
+                                              slab_rc)
 
 
 def test_shard_covers_batch():
@@ -103,3 +104,83 @@ def test_slab_all_to_all_matches_single_process(world):
         p.join(timeout=120)
         assert p.exitcode == 0
     assert all(results.values()), results
+
+
+def test_halo_plan_c5():
+    """c5 (16384^2, S=25, K=7) over 8 ranks: whole segments per rank, rows
+    tile the image, halos come from the neighbours only."""
+    p = (25, 7, 25.0)
+    plans = [HaloPlan(16384, 16384, 8, r, p) for r in range(8)]
+    assert plans[0].nseg % 8 == 0
+    rows = [pl.rows for pl in plans]
+    assert rows[0][0] == 0 and rows[-1][1] == 16384
+    assert all(a[1] == b[0] for a, b in zip(rows, rows[1:]))
+    assert max(b - a for a, b in rows) - min(b - a for a, b in rows) <= 600
+    for r, pl in enumerate(plans):
+        lo, hi = pl.window_rows
+        assert lo <= pl.rows[0] and hi >= pl.rows[1]
+        srcs = {s for s, d, _, _ in pl.transfers() if d == r}
+        assert srcs <= {r - 1, r + 1}
+        assert pl.halo_bytes() < 16 * 2**20  # vs 117 MB for the all-to-all
+    # the plan is symmetric: every rank derives the same transfer list
+    assert all(pl.transfers() == plans[0].transfers() for pl in plans)
+
+
+def _halo_worker(rank, world, port, H, W, params, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    os.environ["PLGPU_SEG"] = "16"  # many segments at a CPU-test size
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import Oracle
+        from paper_1407_2343_b200 import col_window, workloads
+
+        orc = Oracle.get()
+        S, K, h = params
+        img = workloads.make_image(H, W, 12, 20.0, seed=11).astype(np.float64)
+        plan = HaloPlan(H, W, world, rank, params)
+
+        def row_pass(x, p, out):
+            out.copy_(torch.from_numpy(orc.row_pass(x.numpy(), S, K, h)))
+
+        def naive_cols(full):
+            return np.stack([orc.nlm_1d(full[:, c], S, K, h, naive=True)
+                             for c in range(full.shape[1])], axis=1)
+
+        def col_pass_window(y, in_lo, H_, a, b, p):
+            # Only the window is real; anything read outside it poisons the
+            # result with NaN (the direct oracle reads exactly what it uses).
+            full = np.full((H_, W), np.nan)
+            full[in_lo:in_lo + y.shape[0]] = y.numpy()
+            _, _, out_lo, out_hi = col_window(H_, a, b, p)
+            return torch.from_numpy(naive_cols(full)[out_lo:out_hi])
+
+        r0, r1 = plan.rows
+        got = halo_rc(torch.from_numpy(img[r0:r1].copy()), params, plan, row_pass=row_pass,
+                      col_pass_window=col_pass_window,
+                      new_buffer=lambda shape: torch.zeros(shape, dtype=torch.float64))
+        want = naive_cols(orc.row_pass(img, S, K, h))[r0:r1]
+        ok = got.shape == want.shape and bool(np.array_equal(got.numpy(), want))
+        out_q.put((rank, ok, len({s for s, d, _, _ in plan.transfers() if d == rank})))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_halo_exchange_matches_single_process(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    H, W = 160, 24
+    params = (4, 1, 30.0)
+    port = _free_port()
+    procs = [ctx.Process(target=_halo_worker, args=(r, world, port, H, W, params, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert all(ok for _, ok, _ in results), results
+    if world >= 4:
+        assert max(n for _, _, n in results) >= 2  # some window spans several owners

@@ -399,6 +399,68 @@ def test_slab_transpose_emulated_bitwise():
         assert np.array_equal(got, want[:, g * (W // G):(g + 1) * (W // G)]), g
 
 
+@pytest.mark.parametrize("S,K", [(10, 3), (15, 5), (25, 7), (4, 1), (12, 2), (6, 9)])
+def test_col_pass_window_bitwise(S, K):
+    """Windowed column pass (halo form): for first, middle, last and full
+    segment ranges, the window's output rows equal the whole-image column pass
+    bit for bit, with the window embedded in NaN guard rows (a read outside
+    pl_col_window's range would poison the output) and the output in a -7
+    guard (a stray write would show)."""
+    rng = np.random.default_rng(S * 10 + K)
+    b, H, W = 2, 2048, 96
+    x = rng.uniform(0, 255, (b, H, W)).astype(np.float32)
+    p = (S, K, 55.0)
+    want = host(pl.nlm_col_pass(dev(x), p))
+    nseg = pl.col_segments(H, p)
+    assert nseg >= 4
+    for a, e in [(0, 1), (1, 3), (nseg - 1, nseg), (0, nseg), (2, nseg - 1)]:
+        in_lo, in_hi, out_lo, out_hi = pl.col_window(H, a, e, p)
+        assert in_lo <= out_lo < out_hi <= in_hi
+        G = 64
+        rows = in_hi - in_lo
+        win = dev(x[:, in_lo:in_hi])
+        outbuf = torch.full((b * (out_hi - out_lo) * W + 2 * 4096,), -7.0, device="cuda")
+        out = outbuf[4096:4096 + b * (out_hi - out_lo) * W].view(b, out_hi - out_lo, W)
+        got = host(pl.nlm_col_pass_window(win, in_lo, H, a, e, p, out=out))
+        assert np.array_equal(got, want[:, out_lo:out_hi]), (a, e)
+        assert (host(outbuf[:4096]) == -7).all() and (host(outbuf[-4096:]) == -7).all()
+        # one image with NaN rows right outside its window (batch 1)
+        one = torch.full((rows + 2 * G, W), float("nan"), device="cuda")
+        one[G:G + rows] = dev(x[0, in_lo:in_hi])
+        got1 = host(pl.nlm_col_pass_window(one[G:G + rows], in_lo, H, a, e, p))
+        assert np.array_equal(got1, want[0, out_lo:out_hi]), (a, e)
+    with pytest.raises(IndexError):  # window too small
+        in_lo, in_hi, _, _ = pl.col_window(H, 1, 2, p)
+        pl.nlm_col_pass_window(dev(x[0, in_lo + 1:in_hi]), in_lo + 1, H, 1, 2, p)
+
+
+@pytest.mark.parametrize("G,S,K", [(4, 10, 3), (8, 25, 7), (3, 15, 5)])
+def test_halo_exchange_emulated_bitwise(G, S, K):
+    """c5's halo-exchange path with G ranks emulated on one GPU (row pass of
+    each rank's rows into its window buffer, the plan's transfers as device
+    copies between the ranks' buffers, windowed column pass): the stitched
+    row slabs equal the single-device RC bit for bit."""
+    from paper_1407_2343_b200.distributed import HaloPlan
+    H, W = 8192, 128
+    h = 60.0
+    img = workloads.make_image(H, W, 40, 25.0, seed=6)
+    want = host(pl.snlm_2d_row_col(dev(img), (S, K, h)))
+    plans = [HaloPlan(H, W, G, r, (S, K, h)) for r in range(G)]
+    ys = []
+    for r, plan in enumerate(plans):
+        (olo, ohi), (wlo, whi) = plan.rows, plan.window_rows
+        y = torch.full((whi - wlo, W), float("nan"), device="cuda")
+        pl.nlm_row_pass(dev(img[olo:ohi]), (S, K, h), out=y[olo - wlo:ohi - wlo])
+        ys.append(y)
+    for s, d, lo, hi in plans[0].transfers():
+        ys[d][lo - plans[d].window_rows[0]:hi - plans[d].window_rows[0]] = \
+            ys[s][lo - plans[s].window_rows[0]:hi - plans[s].window_rows[0]]
+    got = np.concatenate([host(pl.nlm_col_pass_window(ys[r], plans[r].window_rows[0], H,
+                                                      *plans[r].segments, (S, K, h)))
+                          for r in range(G)])
+    assert np.array_equal(got, want)
+
+
 def test_guard_bands_no_stray_access():
     """Stand-in for compute-sanitizer (closed on this pool): every kernel path runs on
     inputs/outputs embedded in NaN guard bands.  A stray read poisons an output with
