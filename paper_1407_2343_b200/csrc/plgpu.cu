@@ -222,6 +222,7 @@ int try_pass2(const plgpu::PassDesc& g, cudaStream_t st) {
   d.S = g.S;
   d.K = g.K;
   d.coef = g.coef;
+  d.scale = g.scale;
   const int64_t images = g.n_lines / g.lines_per_img;
   d.total_warps = images * d.groups_per_img * d.nseg;
   const auto a16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
@@ -290,6 +291,7 @@ int run_pass(plgpu::PassDesc g, const pl_params& p, cudaStream_t st) {
   g.S = std::min<int32_t>(p.search_radius, g.n - 1);
   g.K = p.patch_radius;
   g.coef = weight_coef(p.h);
+  g.scale = static_cast<float>(std::sqrt(1.4426950408889634) / p.h);
   g.seg_len = segment_length(g.n, g.S);
   if (g.nseg <= 0) {  // whole lines (windowed passes preset seg_begin / nseg)
     g.seg_begin = 0;

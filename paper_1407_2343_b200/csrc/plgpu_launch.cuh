@@ -47,10 +47,6 @@ void launch_band(const BandDesc& g, cudaStream_t st) {
   distance_band_kernel<ST, T><<<(unsigned)((work + 127) / 128), 128, 0, st>>>(g);
 }
 
-// Compile-time patch radius served by the single-ring form for this search
-// radius (the configs' (K, S) pairs), or -1.
-constexpr int fixed_k_for(int ST) { return ST < 0 ? ST : -1; }  // single-ring form disabled: spills
-
 template <int ST, int KT>
 void launch_pass2_k(const Pass2Desc& g, bool rows, cudaStream_t st) {
   constexpr int L = pass2_lines(ST);
@@ -66,11 +62,7 @@ void launch_pass2_k(const Pass2Desc& g, bool rows, cudaStream_t st) {
 
 template <int ST>
 void launch_pass2(const Pass2Desc& g, bool rows, cudaStream_t st) {
-  constexpr int KF = fixed_k_for(ST);
-  if constexpr (KF >= 0) {
-    if (g.K == KF && g.S == ST) return launch_pass2_k<ST, KF>(g, rows, st);
-  }
-  launch_pass2_k<ST, -1>(g, rows, st);
+  launch_pass2_k<ST, -1>(g, rows, st);  // runtime K (K <= 7)
 }
 
 template <int ST>

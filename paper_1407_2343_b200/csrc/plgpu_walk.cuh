@@ -11,10 +11,14 @@
 //
 // (PatchLift: banded_kernel.cpp:46-62 runs the same recursion on F-bar and
 // forms d = F(i,i)+F(j,j)-2F(i,j) at :74-84; here the recursion runs directly
-// on the squared differences, so d >= 0 by construction and integer inputs
-// give exact integer distances in fp32: every partial sum is < 2^24 for K<=127).
-// Each unique pair (i, i+k) is weighted ONCE, w = 2^(c*d), c = -log2(e)/h^2
-// (weight(), nlm.cpp:116-118), and feeds both endpoints:
+// on the squared differences, so d >= 0 by construction).  The filter runs
+// it on PRESCALED samples e' = s e, s = sqrt(log2 e)/h (fp32, from double on
+// the host), so d' = d log2(e)/h^2 up to rounding and the weight
+// w = exp(-d/h^2) (weight(), nlm.cpp:116-118) is one MUFU.EX2 of -d' -- no
+// per-pair multiply.  The distance exports (distance_band_kernel) run the
+// recurrence on the raw samples, where integer inputs give exact integer
+// distances (every partial sum < 2^24 for K <= 127).
+// Each unique pair (i, i+k) is weighted ONCE and feeds both endpoints:
 //
 //     num[i] += w f[i+k]; den[i] += w;  num[i+k] += w f[i]; den[i+k] += w
 //
@@ -55,6 +59,7 @@ struct PassDesc {
   int32_t seg_len;  // C
   int32_t nseg;     // segments processed (ceil(n / C) unless windowed)
   int32_t seg_begin;  // index of the first processed segment (windowed passes)
+  float scale;        // sqrt(log2 e) / h: distance-side sample prescale
   int32_t S;        // effective search radius, <= template S, <= n-1
   int32_t K;        // patch radius
   float coef;       // -log2(e) / h^2
@@ -66,16 +71,17 @@ __device__ __forceinline__ float ex2_approx(float x) {
   return y;
 }
 
-// num / den for the filter output: one MUFU.RCP plus one correction step
-// q' = q + r (num - den q) (Markstein).  When the true quotient is
-// representable (e.g. constant inputs: num = m c, den = m) it is returned
-// exactly; otherwise the result is within one ulp of the IEEE quotient.
-// Both walkers use it, so their outputs stay bitwise equal.
+// num / den for the filter output: one MUFU.RCP and a multiply (within ~2 ulp
+// of the IEEE quotient).  Every walker clamps the quotient into the range of
+// the samples it walked, which is what makes constant inputs exact fixpoints
+// and keeps outputs inside the convex hull (acceptance_main.cpp:256-283); a
+// Newton/Markstein correction step bought nothing on top of the clamp and
+// cost ~2%.  All walkers use it, so their outputs stay
+// bitwise equal.
 __device__ __forceinline__ float div_fix(float num, float den) {
   float r;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(den));
-  const float q = num * r;
-  return fmaf(fmaf(-den, q, num), r, q);
+  return num * r;
 }
 
 // Half-sample mirror (core_types.cpp:71-88) extended by a clamp: positions
@@ -96,7 +102,7 @@ __device__ __forceinline__ void walk_segment(const PassDesc& g, const float* __r
   const int n = g.n;
   const int S = EDGE ? g.S : ST;
   const int K = g.K;
-  const float coef = g.coef;
+  const float sc = g.scale;  // distance-side samples are prescaled: d' = -c d
   const int i0 = max(0, s0 - S);
   const int T = s1 - i0;
 
@@ -104,6 +110,9 @@ __device__ __forceinline__ void walk_segment(const PassDesc& g, const float* __r
     if (EDGE) p = mirror_pos(p, n);
     return __ldg(src + (int64_t)p * ps);
   };
+  // __fmul_rn: the scaled sample is rounded once, never contracted into the
+  // difference that consumes it (all walkers must round identically).
+  auto lds = [&](int p) -> float { return __fmul_rn(ld(p), sc); };
 
   float fr[R], nr[R], orr[R];  // rings: f[i+q], e[i+K+q], e[i-1-K+q]
   float d[R];                  // d[k], k = 1..ST (d[0] unused)
@@ -118,18 +127,18 @@ __device__ __forceinline__ void walk_segment(const PassDesc& g, const float* __r
     fr[q] = ld(i0 + q);
     lo = fminf(lo, fr[q]);
     hi = fmaxf(hi, fr[q]);
-    nr[q] = ld(i0 + K + q);
-    orr[q] = ld(i0 - 1 - K + q);
+    nr[q] = lds(i0 + K + q);
+    orr[q] = lds(i0 - 1 - K + q);
     an[q] = 0.f;
     ad[q] = 0.f;
     d[q] = 0.f;
   }
   // Anchor: d_k(i0-1) by a direct (2K+1)-term sum, t ascending.
   for (int t = -K; t <= K; ++t) {
-    const float a = ld(i0 - 1 + t);
+    const float a = lds(i0 - 1 + t);
 #pragma unroll
     for (int k = 1; k <= ST; ++k) {
-      const float df = a - ld(i0 - 1 + t + k);
+      const float df = a - lds(i0 - 1 + t + k);
       d[k] = fmaf(df, df, d[k]);
     }
   }
@@ -148,8 +157,8 @@ __device__ __forceinline__ void walk_segment(const PassDesc& g, const float* __r
       // Entering samples for step s+1 (prefetched one step ahead): the ring
       // slot r advances by R = ST+1 positions.
       const float tf = ld(i + 1 + ST);
-      const float tn = ld(i + 1 + K + ST);
-      const float to = ld(i - K + ST);
+      const float tn = lds(i + 1 + K + ST);
+      const float to = lds(i - K + ST);
       const float an_ = nr[r], ao = orr[r], fi = fr[r];
       const int kmax = EDGE ? min(S, n - 1 - i) : ST;
       float num = an[r] + fi;  // j-side contributions so far + centre (w = 1)
@@ -162,7 +171,7 @@ __device__ __forceinline__ void walk_segment(const PassDesc& g, const float* __r
         const float dq = ao - orr[rk];
         dk = fmaf(-dq, dq, dk);
         d[k] = dk;
-        float w = ex2_approx(coef * dk);
+        float w = ex2_approx(-dk);
         if (EDGE) w = (k <= kmax) ? w : 0.f;
         num = fmaf(w, fr[rk], num);
         den += w;

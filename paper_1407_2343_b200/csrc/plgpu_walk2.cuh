@@ -1,8 +1,8 @@
 // plgpu_walk2.cuh -- the production PatchLift-NLM pass kernel (sm_100a).
 //
-// Same per-line arithmetic as plgpu_walk.cuh (anchor at i0-1, moving-sum
-// update (2), one ex2 per unique pair, both endpoints accumulated, IEEE
-// division, range clamp) -- the two kernels give bitwise-identical outputs --
+// Same per-line arithmetic as plgpu_walk.cuh (prescaled samples, anchor at
+// i0-1, moving-sum update (2), one ex2 per unique pair, both endpoints
+// accumulated, rcp division, range clamp) -- the two kernels give bitwise-identical outputs --
 // but organised for the B200:
 //
 //  * A warp owns LW = 32*LINES lines x one segment.  With LINES = 2 every lane
@@ -52,10 +52,12 @@ struct VecOps<1> {
   static __device__ __forceinline__ V splat(float x) { return x; }
   static __device__ __forceinline__ V add(V a, V b) { return a + b; }
   static __device__ __forceinline__ V sub(V a, V b) { return a - b; }
-  static __device__ __forceinline__ V mul(V a, V b) { return a * b; }
+  static __device__ __forceinline__ V mul(V a, V b) { return __fmul_rn(a, b); }  // never contracted
+  static __device__ __forceinline__ V scale(V a, float s) { return __fmul_rn(a, s); }
   static __device__ __forceinline__ V fma(V a, V b, V c) { return fmaf(a, b, c); }
   static __device__ __forceinline__ V fms(V a, V b, V c) { return fmaf(-a, b, c); }  // c - a*b
   static __device__ __forceinline__ V ex2(V a) { return ex2_approx(a); }
+  static __device__ __forceinline__ V ex2n(V a) { return ex2_approx(-a); }
   static __device__ __forceinline__ V zero_if(bool z, V a) { return z ? 0.f : a; }
   static __device__ __forceinline__ float lo(V a) { return a; }
   static __device__ __forceinline__ float hi(V a) { return a; }
@@ -100,6 +102,20 @@ struct VecOps<2> {
     f2_split(a, x, y);
     return f2_make(ex2_approx(x), ex2_approx(y));
   }
+  // Sample prescale as two scalar mul.rn: ptxas contracts a packed
+  // mul.rn.f32x2 into a following sub.rn.f32x2 (one FFMA2, one rounding less)
+  // whenever the product has a single use, which would make the rounding of
+  // a walker depend on its schedule.  Scalar mul.rn is never contracted.
+  static __device__ __forceinline__ V scale(V a, float s) {
+    float x, y;
+    f2_split(a, x, y);
+    return f2_make(__fmul_rn(x, s), __fmul_rn(y, s));
+  }
+  static __device__ __forceinline__ V ex2n(V a) {  // 2^-a (negation folds into MUFU)
+    float x, y;
+    f2_split(a, x, y);
+    return f2_make(ex2_approx(-x), ex2_approx(-y));
+  }
   static __device__ __forceinline__ V zero_if(bool z, V a) {
     V o;
     o.r = z ? 0ull : a.r;
@@ -125,8 +141,7 @@ struct VecOps<2> {
   // packed div_fix (same arithmetic per half)
   static __device__ __forceinline__ V div(V n, V d) {
     const V r = rcp(d);
-    const V q = mul(n, r);
-    return fma(fms(d, q, n), r, q);
+    return mul(n, r);
   }
   static __device__ __forceinline__ V lds(const float* p) {
     V o;
@@ -164,6 +179,7 @@ struct Pass2Desc {
   int32_t groups_per_img;
   int32_t n, seg_len, nseg, S, K;
   int32_t seg_begin;  // first processed segment (windowed passes; nseg counts from it)
+  float scale;        // sqrt(log2 e) / h: distance-side sample prescale
   int32_t vec16;  // column pass: 16-byte copies legal (aligned, full line groups)
   int64_t total_warps;
   float coef;
@@ -194,16 +210,9 @@ __device__ __forceinline__ int swz(int l, int u) {
 // steps before first use: wait_group(16) at the top of each step suffices,
 // and the slot it overwrites (chunk floor(s/16)-2) was last read two chunks
 // earlier (requires 2K < 16).
-// Single-ring period for compile-time K: smallest multiple of S+1 covering the
-// 2K+S+2 live positions.
-__host__ __device__ constexpr int ring_period(int ST, int KT) {
-  return ((2 * KT + ST + 2 + ST) / (ST + 1)) * (ST + 1);
-}
-
-// KT >= 0: patch radius fixed at compile time, ONE sample ring of period
-// ring_period(ST, KT) (the body unrolls P steps; one LDS per step).
-// KT < 0: runtime K, three rings of S+1 (entering-term partners, leaving-term
-// partners, f values; three LDS per step).
+// KT >= 0: patch radius fixed at compile time; KT < 0: runtime K.  Three
+// register rings of S+1 samples (f values, entering-term partners,
+// leaving-term partners); three LDS per step.
 template <int ST, int KT, int LINES, bool ROWS, bool EDGE>
 __device__ __forceinline__ void walk2(const Pass2Desc& g, float* ring, const int lane,
                                       const int64_t wid) {
@@ -211,9 +220,7 @@ __device__ __forceinline__ void walk2(const Pass2Desc& g, float* ring, const int
   using V = typename Ops::V;
   constexpr int LW = 32 * LINES;
   constexpr int R = ST + 1;
-  constexpr bool ONE = KT >= 0;
-  constexpr int P = ONE ? ring_period(ST, KT) : R;  // body length (steps)
-  constexpr int NRING = ONE ? P : R;
+  constexpr int P = R;  // body length (steps)
   float* oring = ring + kSR * LW;
 
   const int seg = g.seg_begin + (int)(wid % g.nseg);
@@ -222,7 +229,7 @@ __device__ __forceinline__ void walk2(const Pass2Desc& g, float* ring, const int
   const int l0 = (int)(grp % g.groups_per_img) * LW;
   const int n = g.n;
   const int S = g.S;
-  const int K = ONE ? KT : g.K;
+  const int K = KT >= 0 ? KT : g.K;
   const int s0 = seg * g.seg_len;
   const int s1 = min(n, s0 + g.seg_len);
   const int i0 = max(0, s0 - S);
@@ -272,11 +279,12 @@ __device__ __forceinline__ void walk2(const Pass2Desc& g, float* ring, const int
   cp_wait<0>();
   __syncwarp();
 
-  // Sample rings.  ONE: sr[u mod P] = sample at ring coordinate u; else
-  // fr/nr/orr[(s+q) mod R] = samples at u = s+1+K+q, s+1+2K+q, s+q.
-  V fr[ONE ? 1 : R], nr[ONE ? 1 : R], orr[ONE ? 1 : R], sr[ONE ? P : 1];
+  // Sample rings fr/nr/orr[(s+q) mod R] = samples at u = s+1+K+q, s+1+2K+q,
+  // s+q; the distance-side rings nr/orr hold prescaled samples (plgpu_walk.cuh).
+  V fr[R], nr[R], orr[R];
   V an[R], ad[R], d[R];
   const V zero = Ops::splat(0.f);
+  auto lds = [&](int u) -> V { return Ops::scale(ld(u), g.scale); };
   float lo0 = 3.402823466e38f, hi0 = -3.402823466e38f, lo1 = lo0, hi1 = hi0;
   auto track = [&](V v) {
     lo0 = fminf(lo0, Ops::lo(v));
@@ -286,31 +294,21 @@ __device__ __forceinline__ void walk2(const Pass2Desc& g, float* ring, const int
   };
 #pragma unroll
   for (int q = 0; q < R; ++q) {
-    if constexpr (!ONE) {
-      fr[q] = ld(q + 1 + K);
-      nr[q] = ld(q + 1 + 2 * K);
-      orr[q] = ld(q);
-    }
+    fr[q] = ld(q + 1 + K);
+    nr[q] = lds(q + 1 + 2 * K);
+    orr[q] = lds(q);
     an[q] = zero;
     ad[q] = zero;
     d[q] = zero;
   }
-  if constexpr (ONE) {
 #pragma unroll
-    for (int q = 0; q < P; ++q) sr[q] = q < ST + 2 * KT + 2 ? ld(q) : zero;
-    // the clamp range covers f at u in [1+K, 1+K+ST] initially, as the 3-ring form
-#pragma unroll
-    for (int q = 0; q <= ST; ++q) track(sr[1 + KT + q]);
-  } else {
-#pragma unroll
-    for (int q = 0; q < R; ++q) track(fr[q]);
-  }
+  for (int q = 0; q < R; ++q) track(fr[q]);
 #pragma unroll 1
   for (int t = 0; t <= 2 * K; ++t) {  // anchor d_k(i0-1), t ascending
-    const V a = ld(t);
+    const V a = lds(t);
 #pragma unroll
     for (int k = 1; k <= ST; ++k) {
-      const V df = Ops::sub(a, ld(t + k));
+      const V df = Ops::sub(a, lds(t + k));
       d[k] = Ops::fma(df, df, d[k]);
     }
   }
@@ -318,7 +316,6 @@ __device__ __forceinline__ void walk2(const Pass2Desc& g, float* ring, const int
 #pragma unroll 1
   for (int j = 0; j < 16; ++j) issue_piece(1, j);
 
-  const V coefv = Ops::splat(g.coef);
   const V one = Ops::splat(1.f);
   const int64_t dst_img = img * g.dst_img_stride;
   const int my_line = l0 + lane * LINES;
@@ -352,34 +349,23 @@ __device__ __forceinline__ void walk2(const Pass2Desc& g, float* ring, const int
       cp_wait<16>();
       __syncwarp();
       // ring refills (shared-memory latency hides behind the step)
-      V tf, tn, to, tsr;
-      if constexpr (ONE) {
-        tsr = ld(s + base);  // first needed at step s+1
-      } else {
-        tf = ld(s + 2 + K + ST);
-        tn = ld(s + base);
-        to = ld(s + 1 + ST);
-      }
-      // sample at ring coordinate s + off, off in [0, 2K+ST+1]
-      auto smp = [&](int off) -> V { return sr[ONE ? (r + off) % P : 0]; };
-      const V an_ = ONE ? smp(1 + 2 * KT) : nr[ra];
-      const V ao = ONE ? smp(0) : orr[ra];
-      const V fi = ONE ? smp(1 + KT) : fr[ra];
+      const V tf = ld(s + 2 + K + ST);
+      const V tn = lds(s + base);
+      const V to = lds(s + 1 + ST);
+      const V an_ = nr[ra], ao = orr[ra], fi = fr[ra];
       const int kmax = EDGE ? min(S, n - 1 - i) : ST;
       V num = Ops::add(an[ra], fi);
       V den = Ops::add(ad[ra], one);
 #pragma unroll
       for (int k = 1; k <= ST; ++k) {
         const int rk = (ra + k) % R;
-        const V pn = ONE ? smp(1 + 2 * KT + k) : nr[rk];
-        const V po = ONE ? smp(k) : orr[rk];
-        const V pf = ONE ? smp(1 + KT + k) : fr[rk];
+        const V pn = nr[rk], po = orr[rk], pf = fr[rk];
         const V dn = Ops::sub(an_, pn);
         V dk = Ops::fma(dn, dn, d[k]);
         const V dq = Ops::sub(ao, po);
         dk = Ops::fms(dq, dq, dk);
         d[k] = dk;
-        V w = Ops::ex2(Ops::mul(dk, coefv));
+        V w = Ops::ex2n(dk);
         if constexpr (EDGE) w = Ops::zero_if(k > kmax, w);
         num = Ops::fma(w, pf, num);
         den = Ops::add(w, den);
@@ -414,15 +400,10 @@ __device__ __forceinline__ void walk2(const Pass2Desc& g, float* ring, const int
       }
       an[ra] = zero;
       ad[ra] = zero;
-      if constexpr (ONE) {
-        sr[(r + ST + 2 * KT + 2) % P] = tsr;
-        track(smp(2 + KT + ST));  // f entering the window of step s+1
-      } else {
-        track(tf);
-        fr[ra] = tf;
-        nr[ra] = tn;
-        orr[ra] = to;
-      }
+      track(tf);
+      fr[ra] = tf;
+      nr[ra] = tn;
+      orr[ra] = to;
       issue_piece((s >> 4) + 2, s & 15);
     }
   }

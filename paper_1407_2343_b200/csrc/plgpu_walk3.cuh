@@ -29,6 +29,7 @@
 
 #include "plgpu_walk2.cuh"
 
+
 namespace plgpu {
 
 constexpr int kNS3 = 4;
@@ -190,6 +191,8 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
   V nr[R], orr[R], d[R];
   F2 frp[PK ? R : 1], acc[PK ? R : 1];
   const V zero = Ops::splat(0.f);
+  const float sv = g.scale;
+  auto sc = [&](V v) -> V { return Ops::scale(v, sv); };  // distance-side sample
   const F2 zero2 = f2_make(0.f, 0.f);
   float lo0 = 3.402823466e38f, hi0 = -3.402823466e38f, lo1 = lo0, hi1 = hi0;
   auto track = [&](V v) {
@@ -200,8 +203,8 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
   };
 #pragma unroll
   for (int q = 0; q < R; ++q) {
-    nr[q] = ld_init(q + 1 + 2 * KT);
-    orr[q] = ld_init(q);
+    nr[q] = sc(ld_init(q + 1 + 2 * KT));
+    orr[q] = sc(ld_init(q));
     d[q] = zero;
     const V f = ld_init(q + 1 + KT);
     if constexpr (PK) {
@@ -216,15 +219,14 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
   }
 #pragma unroll
   for (int t = 0; t <= 2 * KT; ++t) {  // anchor d_k(i0-1), t ascending
-    const V a = ld_init(t);
+    const V a = sc(ld_init(t));
 #pragma unroll
     for (int k = 1; k <= ST; ++k) {
-      const V df = Ops::sub(a, ld_init(t + k));
+      const V df = Ops::sub(a, sc(ld_init(t + k)));
       d[k] = Ops::fma(df, df, d[k]);
     }
   }
 
-  const V coefv = Ops::splat(g.coef);
   const V one = Ops::splat(1.f);
   const int64_t dst_img = img * g.dst_img_stride;
   const int my_line = l0 + lane * LINES;
@@ -273,7 +275,7 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
             const float dq = ao - orr[rk];
             dk = fmaf(-dq, dq, dk);
             d[k] = dk;
-            float w = ex2_approx(dk * g.coef);
+            float w = ex2_approx(-dk);
             if constexpr (MASK) w = k > kmax ? 0.f : w;
             const F2 ww = f2_make(w, w);
             nd = O2::fma(frp[rk], ww, nd);  // num += w f_{i+k}; den += w
@@ -295,7 +297,7 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
             const V dq = Ops::sub(ao, orr[rk]);
             dk = Ops::fms(dq, dq, dk);
             d[k] = dk;
-            V w = Ops::ex2(Ops::mul(dk, coefv));
+            V w = Ops::ex2n(dk);
             if constexpr (MASK) w = Ops::zero_if(k > kmax, w);
             num = Ops::fma(w, fr[rk], num);
             den = Ops::add(w, den);
@@ -319,11 +321,11 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
         }
         // refill slot r in place: first read at step r+1's last offset
         const V fnew = at(r, 2 + KT + ST);
+        track(fnew);
         if constexpr (PK) frp[r] = f2_make(Ops::lo(fnew), 1.f);
         else fr[r] = fnew;
-        nr[r] = at(r, BASE);
-        orr[r] = at(r, 1 + ST);
-        track(fnew);
+        nr[r] = sc(at(r, BASE));
+        orr[r] = sc(at(r, 1 + ST));
       }
     };
     if constexpr (MODE == 1) {
