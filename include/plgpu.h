@@ -182,6 +182,18 @@ int pl_distance_band_i32(const float* src, int32_t* band, int64_t n_lines, int32
 int pl_banded_kernel_f64(const double* src, double* band, int64_t n_lines, int32_t n, int64_t ld,
                          int32_t search_radius, int32_t patch_radius, void* stream);
 
+/* ---- fidelity metrics (metrics.cpp:98-158) ---
+ * For each of `batch` image pairs [rows][cols] (device buffers, fp32 or fp64):
+ * out[3*b + 0] = mse, out[3*b + 1] = psnr_db (+inf for identical images),
+ * out[3*b + 2] = ssim (11x11 Gaussian window, sigma 1.5, valid positions).
+ * `out` is a device buffer of 3*batch doubles.  Images smaller than 11x11
+ * have no SSIM (the reference throws "image smaller than the 11x11
+ * structural window"): their ssim is NaN, mse and psnr are still valid. */
+int pl_image_metrics_f32(const float* a, const float* b, int32_t batch, int32_t rows, int32_t cols,
+                         double* out, void* stream);
+int pl_image_metrics_f64(const double* a, const double* b, int32_t batch, int32_t rows,
+                         int32_t cols, double* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

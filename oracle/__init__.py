@@ -72,6 +72,15 @@ class _Base:
             raise OracleError(rc, msg.decode() if msg else "")
 
 
+def _metrics(obj, fn, a, b):
+    a, b = _f64(a), _f64(b)
+    if a.shape != b.shape or a.ndim != 2:
+        raise ValueError("expected two images of equal [rows, cols] shape")
+    out = np.empty(3)
+    obj._check(fn(_ptr(a), _ptr(b), C.c_int(a.shape[0]), C.c_int(a.shape[1]), _ptr(out)))
+    return float(out[0]), float(out[1]), float(out[2])
+
+
 class Oracle(_Base):
     """My C restatement (double precision)."""
 
@@ -140,6 +149,10 @@ class Oracle(_Base):
 
     def weight(self, rho_sq, h):
         return self.lib.orc_weight(rho_sq, h)
+
+    def metrics(self, a, b):
+        """(mse, psnr_db, ssim) of two [rows, cols] images (metrics.cpp:98-158)."""
+        return _metrics(self, getattr(self.lib, self._prefix + "metrics"), a, b)
 
     def nlm_1d(self, f, S, K, h, naive=False, ops=None):
         f = _f64(f)
@@ -252,6 +265,10 @@ class Reference(_Base):
 
     def weight(self, rho_sq, h):
         return self.lib.ref_weight(rho_sq, h)
+
+    def metrics(self, a, b):
+        """(mse, psnr_db, ssim) of two [rows, cols] images (metrics.cpp:98-158)."""
+        return _metrics(self, getattr(self.lib, self._prefix + "metrics"), a, b)
 
     def nlm_1d(self, f, S, K, h, naive=False, ops=None):
         f = _f64(f)

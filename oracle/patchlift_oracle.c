@@ -339,3 +339,79 @@ int orc_snlm(const double* img, int rows, int cols, int S, int K, double h, doub
   free(cr_img);
   return rc;
 }
+
+/* ---- image fidelity metrics (metrics.cpp:12-150) ------------------------ */
+/* 11-tap Gaussian window, sigma 1.5, normalised: metrics.cpp:14-17,25-37 */
+static void ssim_kernel(double k[11]) {
+  double total = 0.0;
+  for (int t = 0; t < 11; ++t) {
+    const double x = t - (11 - 1) / 2;
+    k[t] = exp(-x * x / (2.0 * 1.5 * 1.5));
+    total += k[t];
+  }
+  for (int t = 0; t < 11; ++t) k[t] /= total;
+}
+
+/* valid-mode separable correlation, rows then columns: metrics.cpp:39-64 */
+static void ssim_blur(const double* src, int h, int w, const double k[11], double* tmp,
+                      double* out) {
+  const int wo = w - 11 + 1, ho = h - 11 + 1;
+  for (int r = 0; r < h; ++r)
+    for (int c = 0; c < wo; ++c) {
+      double s = 0.0;
+      for (int t = 0; t < 11; ++t) s += k[t] * src[(size_t)r * w + c + t];
+      tmp[(size_t)r * wo + c] = s;
+    }
+  for (int r = 0; r < ho; ++r)
+    for (int c = 0; c < wo; ++c) {
+      double s = 0.0;
+      for (int t = 0; t < 11; ++t) s += k[t] * tmp[(size_t)(r + t) * wo + c];
+      out[(size_t)r * wo + c] = s;
+    }
+}
+
+/* mse (metrics.cpp:98-106), psnr (:108-114), ssim (:116-150) of one image
+ * pair; out[0..2] = mse, psnr_db, ssim.  psnr is +inf for identical images. */
+int orc_metrics(const double* a, const double* b, int rows, int cols, double* out) {
+  if (rows < 11 || cols < 11) return fail(1, "image smaller than the 11x11 structural window");
+  const size_t n = (size_t)rows * cols;
+  double acc = 0.0;
+  for (size_t k = 0; k < n; ++k) {
+    const double diff = a[k] - b[k];
+    acc += diff * diff;
+  }
+  const double m = acc / (double)n;
+  out[0] = m;
+  out[1] = m == 0.0 ? INFINITY : 10.0 * log10(255.0 * 255.0 / m);
+  const int wo = cols - 10, ho = rows - 10;
+  const size_t no = (size_t)ho * wo;
+  double* buf = (double*)malloc(sizeof(double) * (3 * n + (size_t)rows * wo + 5 * no));
+  if (!buf) return fail(3, "out of memory");
+  double *xx = buf, *yy = xx + n, *xy = yy + n, *tmp = xy + n, *mu_x = tmp + (size_t)rows * wo;
+  double *mu_y = mu_x + no, *e_xx = mu_y + no, *e_yy = e_xx + no, *e_xy = e_yy + no;
+  for (size_t k = 0; k < n; ++k) {
+    xx[k] = a[k] * a[k];
+    yy[k] = b[k] * b[k];
+    xy[k] = a[k] * b[k];
+  }
+  double kern[11];
+  ssim_kernel(kern);
+  ssim_blur(a, rows, cols, kern, tmp, mu_x);
+  ssim_blur(b, rows, cols, kern, tmp, mu_y);
+  ssim_blur(xx, rows, cols, kern, tmp, e_xx);
+  ssim_blur(yy, rows, cols, kern, tmp, e_yy);
+  ssim_blur(xy, rows, cols, kern, tmp, e_xy);
+  const double C1 = (0.01 * 255.0) * (0.01 * 255.0), C2 = (0.03 * 255.0) * (0.03 * 255.0);
+  double total = 0.0;
+  for (size_t k = 0; k < no; ++k) {
+    const double mx = mu_x[k], my = mu_y[k];
+    const double var_x = e_xx[k] - mx * mx;
+    const double var_y = e_yy[k] - my * my;
+    const double cov = e_xy[k] - mx * my;
+    total += ((2.0 * mx * my + C1) * (2.0 * cov + C2)) /
+             ((mx * mx + my * my + C1) * (var_x + var_y + C2));
+  }
+  out[2] = total / (double)no;
+  free(buf);
+  return 0;
+}

@@ -14,6 +14,7 @@
 //   ref_image_filter       -> nlm_row_pass / nlm_col_pass / snlm_2d_row_col /
 //                             snlm_2d_col_row / snlm_2d / nlm_2d_naive  nlm.cpp:168-253
 //   ref_dump_kernel_csv    -> patchlift::dump_kernel_csv           banded_kernel.cpp:110-120
+//   ref_metrics            -> patchlift::compare_images (mse, psnr, ssim)  metrics.cpp:98-158
 //
 // Status codes: 0 ok, 1 patchlift::ValidationError, 2 std::out_of_range,
 // 3 any other exception.  The message is kept per thread (ref_last_error).
@@ -27,6 +28,7 @@
 
 #include "patchlift/banded_kernel.hpp"
 #include "patchlift/core_types.hpp"
+#include "patchlift/metrics.hpp"
 #include "patchlift/nlm.hpp"
 
 namespace {
@@ -150,6 +152,18 @@ int ref_image_filter(int op, const double* img, int rows, int cols, int S, int K
     }
     std::memcpy(out, r.data.data(), r.data.size() * sizeof(double));
     put_ops(ops, ops4);
+  });
+}
+
+int ref_metrics(const double* a, const double* b, int rows, int cols, double* out3) {
+  return guarded([&] {
+    const std::size_t cnt = static_cast<std::size_t>(rows > 0 ? rows : 0) * (cols > 0 ? cols : 0);
+    const patchlift::Image2D x(rows, cols, std::vector<double>(a, a + cnt));
+    const patchlift::Image2D y(rows, cols, std::vector<double>(b, b + cnt));
+    const patchlift::MetricReport m = patchlift::compare_images(x, y);
+    out3[0] = m.mse;
+    out3[1] = m.psnr_db;
+    out3[2] = m.ssim;
   });
 }
 

@@ -35,7 +35,7 @@ EXPORTS = [
     "pl_snlm_2d_col_row", "pl_snlm_2d", "pl_snlm_2d_row_col_host", "pl_nlm_2d_naive",
     "pl_device_alloc", "pl_device_free", "pl_copy_to_device", "pl_copy_to_host",
     "pl_synchronize", "pl_distance_band_f32", "pl_distance_band_i32", "pl_banded_kernel_f64",
-    "pl_col_window", "pl_nlm_col_pass_window",
+    "pl_col_window", "pl_nlm_col_pass_window", "pl_image_metrics_f32", "pl_image_metrics_f64",
 ]
 
 
@@ -95,6 +95,8 @@ def lib() -> C.CDLL:
             "pl_nlm_col_pass": ([vp, vp, i32, i32, i32, P, vp], C.c_int),
             "pl_nlm_row_pass_blocked": ([vp, vp, i32, i32, i32, i32, P, vp], C.c_int),
             "pl_col_window": ([i32, i32, i32, P] + [C.POINTER(i32)] * 4, C.c_int),
+            "pl_image_metrics_f32": ([vp, vp, i32, i32, i32, vp, vp], C.c_int),
+            "pl_image_metrics_f64": ([vp, vp, i32, i32, i32, vp, vp], C.c_int),
             "pl_nlm_col_pass_window": ([vp, i32, i32, vp, i32, i32, i32, i32, i32, P, vp],
                                        C.c_int),
             "pl_workspace_bytes": ([i32, i32, i32, i32], C.c_size_t),
@@ -340,6 +342,24 @@ def banded_kernel_f64(x, S: int, K: int):
     _check(lib().pl_banded_kernel_f64(x.data_ptr(), band.data_ptr(), lines, n, n, int(S), int(K),
                                       _stream(x)))
     return band
+
+
+def image_metrics(a, b):
+    """(mse, psnr_db, ssim) per image pair of device tensors [rows, cols] or
+    [batch, rows, cols] (float32 or float64): a [batch, 3] float64 tensor."""
+    import torch
+    _dev(a)
+    _dev(b, a.dtype)
+    if a.shape != b.shape:
+        raise ValidationError("image dimensions do not match")
+    bt, r, c = _image_dims(a)
+    out = torch.empty((bt, 3), dtype=torch.float64, device=a.device)
+    fn = {torch.float32: lib().pl_image_metrics_f32,
+          torch.float64: lib().pl_image_metrics_f64}.get(a.dtype)
+    if fn is None:
+        raise TypeError("expected float32 or float64 images")
+    _check(fn(a.data_ptr(), b.data_ptr(), bt, r, c, out.data_ptr(), _stream(a)))
+    return out
 
 
 def h_for(sigma: float, K: int) -> float:

@@ -1,5 +1,5 @@
 // patchlift_dropin.cpp -- libpatchlift_b200: the reference's C++ API
-// (proj/include/patchlift/{core_types,banded_kernel,nlm,op_counter}.hpp)
+// (proj/include/patchlift/{core_types,banded_kernel,nlm,op_counter,metrics}.hpp)
 // re-implemented over the C ABI in plgpu.h, so a caller of the reference
 // links against this library unchanged and its filters run on the B200.
 //
@@ -16,14 +16,17 @@
 //    too (nlm.cpp:13-17).
 #include <cmath>
 #include <cstdio>
+#include <limits>
 #include <memory>
 #include <ostream>
+#include <random>
 #include <stdexcept>
 #include <string>
 #include <vector>
 
 #include "patchlift/banded_kernel.hpp"
 #include "patchlift/core_types.hpp"
+#include "patchlift/metrics.hpp"
 #include "patchlift/nlm.hpp"
 #include "plgpu.h"
 
@@ -347,6 +350,69 @@ Image2D snlm_2d(const Image2D& img, const NlmParams& p, OpCounter* ops, int thre
   }
   if (identity_rows(img, p) && identity_cols(img, p)) return img;
   return run_image(img, p, Op::Snlm, nullptr);
+}
+
+// ---- metrics.hpp ------------------------------------------------------------
+namespace {
+
+void require_same_dims(const Image2D& a, const Image2D& b) {  // metrics.cpp:19-23
+  if (a.rows != b.rows || a.cols != b.cols) throw ValidationError("image dimensions do not match");
+}
+
+MetricReport device_metrics(const Image2D& a, const Image2D& b) {
+  require_same_dims(a, b);
+  const std::size_t cnt = a.data.size();
+  DeviceBuffer<double> da(cnt), db(cnt), out(3);
+  da.upload(a.data.data());
+  db.upload(b.data.data());
+  check(pl_image_metrics_f64(da.get(), db.get(), 1, a.rows, a.cols, out.get(), nullptr));
+  double v[3];
+  out.download(v);
+  return MetricReport{v[0], v[1], v[2]};
+}
+
+std::string format_sig6(double v) {  // metrics.cpp:66-73
+  if (std::isinf(v)) return v > 0 ? "inf" : "-inf";
+  char buf[48];
+  std::snprintf(buf, sizeof(buf), "%#.6g", v);
+  return buf;
+}
+
+void require_ssim_window(const Image2D& a) {  // metrics.cpp:118-120
+  if (a.rows < 11 || a.cols < 11)
+    throw ValidationError("image smaller than the 11x11 structural window");
+}
+
+}  // namespace
+
+std::string MetricReport::to_line() const {
+  return "mse=" + format_sig6(mse) + " psnr_db=" + format_sig6(psnr_db) + " ssim=" + format_sig6(ssim);
+}
+
+Image2D add_awgn(const Image2D& img, double sigma, std::uint64_t seed) {  // metrics.cpp:83-97
+  if (!(sigma >= 0.0)) throw ValidationError("noise sigma must be nonnegative");
+  if (sigma == 0.0) return img;
+  Image2D out(img.rows, img.cols);
+  std::mt19937_64 rng(seed);
+  std::normal_distribution<double> gauss(0.0, sigma);
+  for (std::size_t k = 0; k < img.data.size(); ++k) out.data[k] = img.data[k] + gauss(rng);
+  return out;
+}
+
+double mse(const Image2D& a, const Image2D& b) { return device_metrics(a, b).mse; }
+
+double psnr(const Image2D& a, const Image2D& b) { return device_metrics(a, b).psnr_db; }
+
+double ssim(const Image2D& a, const Image2D& b) {
+  require_same_dims(a, b);
+  require_ssim_window(a);
+  return device_metrics(a, b).ssim;
+}
+
+MetricReport compare_images(const Image2D& ref, const Image2D& test) {
+  require_same_dims(ref, test);
+  require_ssim_window(ref);
+  return device_metrics(ref, test);
 }
 
 }  // namespace patchlift

@@ -15,6 +15,7 @@
 #include "plgpu.h"
 #include "plgpu_aux.cuh"
 #include "plgpu_launch.cuh"
+#include "plgpu_metrics.cuh"
 #include "plgpu_walk.cuh"
 
 namespace {
@@ -792,3 +793,63 @@ int pl_synchronize(void) {
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Fidelity metrics (metrics.cpp:98-158) on the device.
+namespace {
+
+plgpu::SsimWindow ssim_window() {  // metrics.cpp:25-37, same libm exp as the reference
+  plgpu::SsimWindow w{};
+  double total = 0.0;
+  for (int t = 0; t < plgpu::kSsimWin; ++t) {
+    const double x = t - (plgpu::kSsimWin - 1) / 2;
+    w.k[t] = std::exp(-x * x / (2.0 * 1.5 * 1.5));
+    total += w.k[t];
+  }
+  for (double& v : w.k) v /= total;
+  return w;
+}
+
+template <typename T>
+int image_metrics(const T* a, const T* b, int32_t batch, int32_t rows, int32_t cols, double* out,
+                  void* stream) {
+  int rc = validate_image(batch, rows, cols);
+  if (!rc) rc = check_ptrs(a, b);
+  if (rc) return rc;
+  if (!out) return set_err(PL_ERR_ARG, "null output buffer");
+  cudaStream_t st = as_stream(stream);
+  // Images under 11x11 have no SSIM (the reference throws); mse/psnr still hold.
+  const bool has_ssim = rows >= plgpu::kSsimWin && cols >= plgpu::kSsimWin;
+  const int wo = has_ssim ? cols - plgpu::kSsimWin + 1 : 0;
+  const int ho = has_ssim ? rows - plgpu::kSsimWin + 1 : 0;
+  const dim3 tiles((wo + plgpu::kSsimTW - 1) / plgpu::kSsimTW, (ho + plgpu::kSsimTH - 1) / plgpu::kSsimTH,
+                   batch);
+  const int64_t ntiles = (int64_t)tiles.x * tiles.y;
+  double* part = nullptr;  // stream-ordered scratch: MSE partials, then SSIM partials
+  const size_t n_mse = (size_t)batch * plgpu::kMseBlocks;
+  PL_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&part),
+                          sizeof(double) * (n_mse + (size_t)batch * ntiles), st));
+  const int64_t n = (int64_t)rows * cols;
+  plgpu::mse_partial_kernel<T><<<dim3(plgpu::kMseBlocks, batch), plgpu::kMetricThreads, 0, st>>>(
+      a, b, n, part);
+  if (has_ssim)
+    plgpu::ssim_partial_kernel<T><<<tiles, plgpu::kMetricThreads, 0, st>>>(a, b, rows, cols,
+                                                                          ssim_window(), part + n_mse);
+  plgpu::metrics_finish_kernel<<<batch, plgpu::kMetricThreads, 0, st>>>(
+      part, part + n_mse, ntiles, n, (int64_t)wo * ho, out);
+  rc = check_launch();
+  PL_CUDA(cudaFreeAsync(part, st));
+  return rc;
+}
+
+}  // namespace
+
+int pl_image_metrics_f32(const float* a, const float* b, int32_t batch, int32_t rows, int32_t cols,
+                         double* out, void* stream) {
+  return image_metrics(a, b, batch, rows, cols, out, stream);
+}
+
+int pl_image_metrics_f64(const double* a, const double* b, int32_t batch, int32_t rows,
+                         int32_t cols, double* out, void* stream) {
+  return image_metrics(a, b, batch, rows, cols, out, stream);
+}

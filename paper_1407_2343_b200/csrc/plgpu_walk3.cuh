@@ -324,8 +324,11 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
         track(fnew);
         if constexpr (PK) frp[r] = f2_make(Ops::lo(fnew), 1.f);
         else fr[r] = fnew;
+        // The leaving-term partner entering now (coordinate s+1+ST) entered
+        // the nr ring 2K+1 steps ago and is still there when 2K < S.
+        if constexpr (2 * KT < ST && ST <= 16) orr[r] = nr[(r + R - 2 * KT - 1) % R];  // (S=25: spills)
+        else orr[r] = sc(at(r, 1 + ST));
         nr[r] = sc(at(r, BASE));
-        orr[r] = sc(at(r, 1 + ST));
       }
     };
     if constexpr (MODE == 1) {

@@ -13,6 +13,7 @@
 
 #include "patchlift/banded_kernel.hpp"
 #include "patchlift/core_types.hpp"
+#include "patchlift/metrics.hpp"
 #include "patchlift/nlm.hpp"
 
 using namespace patchlift;
@@ -36,6 +37,29 @@ static std::string error_of(Fn&& fn) {
     return "out_of_range";
   }
   return "";
+}
+
+// Direct (non-separable) windowed SSIM, written independently of the library's
+// separable blur: every valid 11x11 window with product weights.
+static double ssim_direct(const Image2D& a, const Image2D& b) {
+  const double C1 = (0.01 * 255.0) * (0.01 * 255.0), C2 = (0.03 * 255.0) * (0.03 * 255.0);
+  double k[11], tot = 0.0;
+  for (int t = 0; t < 11; ++t) tot += (k[t] = std::exp(-(t - 5.0) * (t - 5.0) / 4.5));
+  for (double& v : k) v /= tot;
+  double sum = 0.0;
+  int cnt = 0;
+  for (int r = 0; r + 11 <= a.rows; ++r)
+    for (int c = 0; c + 11 <= a.cols; ++c, ++cnt) {
+      double mx = 0, my = 0, xx = 0, yy = 0, xy = 0;
+      for (int u = 0; u < 11; ++u)
+        for (int v = 0; v < 11; ++v) {
+          const double w = k[u] * k[v], x = a.at(r + u, c + v), y = b.at(r + u, c + v);
+          mx += w * x, my += w * y, xx += w * x * x, yy += w * y * y, xy += w * x * y;
+        }
+      const double vx = xx - mx * mx, vy = yy - my * my, cv = xy - mx * my;
+      sum += ((2 * mx * my + C1) * (2 * cv + C2)) / ((mx * mx + my * my + C1) * (vx + vy + C2));
+    }
+  return sum / cnt;
 }
 
 static Image2D random_image(int r, int c, std::mt19937_64& rng) {
@@ -150,6 +174,39 @@ int main() {
       const auto mm = std::minmax_element(img.data.begin(), img.data.end());
       for (const double v : snlm_2d(img, p).data) CHECK(v >= *mm.first && v <= *mm.second);
     }
+  }
+  // metrics (device, fp64): the cases of metrics_test.cpp:73-170
+  {
+    Image2D a(16, 16, 100.0), b(16, 16, 116.0);
+    CHECK(mse(a, b) == 256.0);
+    CHECK(std::abs(psnr(a, b) - 10.0 * std::log10(65025.0 / 256.0)) <= 1e-12 * 24.0);
+    std::mt19937_64 rng(41);
+    const Image2D x = random_image(20, 18, rng);
+    CHECK(mse(x, x) == 0.0 && std::isinf(psnr(x, x)) && psnr(x, x) > 0 && ssim(x, x) == 1.0);
+    CHECK(compare_images(x, x).to_line() == "mse=0.00000 psnr_db=inf ssim=1.00000");
+    const Image2D zeros(16, 16, 0.0), full(16, 16, 255.0);
+    const double c1 = (0.01 * 255.0) * (0.01 * 255.0);
+    CHECK(std::abs(ssim(zeros, full) - c1 / (255.0 * 255.0 + c1)) <= 1e-12 * 1e-4);
+    Image2D y = x;
+    std::normal_distribution<double> g(0.0, 12.0);
+    for (double& v : y.data) v += g(rng);
+    const double s = ssim(x, y), want = ssim_direct(x, y);
+    CHECK(std::abs(s - want) <= 1e-12 * std::abs(want) && s < 1.0 && s > 0.0);
+    CHECK(ssim(x, y) == ssim(y, x));
+    const MetricReport rep = compare_images(x, y);
+    CHECK(rep.mse == mse(x, y) && rep.psnr_db == psnr(x, y) && rep.ssim == s);
+    CHECK(error_of([&] { mse(Image2D(16, 16, 1.0), Image2D(16, 15, 1.0)); }) ==
+          "image dimensions do not match");
+    CHECK(error_of([&] { ssim(Image2D(10, 16, 1.0), Image2D(10, 16, 1.0)); }) ==
+          "image smaller than the 11x11 structural window");
+    CHECK(ssim(Image2D(11, 11, 1.0), Image2D(11, 11, 1.0)) == 1.0);
+    CHECK(mse(Image2D(3, 4, 1.0), Image2D(3, 4, 3.0)) == 4.0);  // any size for mse
+    MetricReport r;
+    r.mse = 256.0, r.psnr_db = 24.0483561, r.ssim = 0.912345678;
+    CHECK(r.to_line() == "mse=256.000 psnr_db=24.0484 ssim=0.912346");
+    const Image2D n1 = add_awgn(a, 5.0, 42), n2 = add_awgn(a, 5.0, 42), n3 = add_awgn(a, 5.0, 43);
+    CHECK(n1.data == n2.data && n1.data != n3.data && add_awgn(a, 0.0, 42).data == a.data);
+    CHECK(error_of([&] { add_awgn(a, -1.0, 42); }) == "noise sigma must be nonnegative");
   }
   std::printf("dropin_check: %d failure(s)\n", g_fail);
   return g_fail;

@@ -63,6 +63,16 @@ def main() -> None:
     band = ref.distance_band(f[:4096], S, K)
     g["c1_dist_head"] = band.astype(np.float64)
 
+    # Fidelity metrics (metrics.cpp:98-158): noisy / filtered image pairs.
+    mrng = np.random.default_rng(77)
+    mcases = [(11, 11), (16, 23), (40, 33), (64, 64)]
+    for t, (r, c) in enumerate(mcases):
+        a = mrng.uniform(0, 255, (r, c)).astype(np.float32).astype(np.float64)
+        b = (a + mrng.normal(0, 12.0, (r, c))).astype(np.float32).astype(np.float64)
+        g[f"m{t}_a"], g[f"m{t}_b"] = a, b
+        g[f"m{t}_metrics"] = np.array(ref.metrics(a, b))
+    g["metric_cases"] = np.array(mcases, dtype=np.float64)
+
     np.savez_compressed(OUT, **g)
     print(f"wrote {OUT}: {len(g)} arrays, {os.path.getsize(OUT) / 1e6:.2f} MB")
 

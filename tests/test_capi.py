@@ -46,7 +46,9 @@ def test_dropin_exports_reference_api():
                "patchlift::extend_symmetric(", "patchlift::transpose(", "patchlift::validate_params(",
                "patchlift::validate_geometry(", "patchlift::weight(", "patchlift::lift_value(",
                "patchlift::Signal1D::Signal1D(", "patchlift::Image2D::Image2D(",
-               "patchlift::BandedKernel::at("]:
+               "patchlift::BandedKernel::at(", "patchlift::mse(", "patchlift::psnr(",
+               "patchlift::ssim(", "patchlift::compare_images(", "patchlift::add_awgn(",
+               "patchlift::MetricReport::to_line"]:
         assert fn in demangled, fn
 
 

@@ -461,6 +461,32 @@ def test_halo_exchange_emulated_bitwise(G, S, K):
     assert np.array_equal(got, want)
 
 
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_image_metrics_vs_oracle(dtype):
+    """Device MSE / PSNR / SSIM (metrics.cpp:98-158) against the oracle on the
+    same inputs: per-pixel quantities are evaluated in the reference's order,
+    only the final sums differ in association (rel 1e-12)."""
+    from oracle import Oracle
+    orc = Oracle.get()
+    rng = np.random.default_rng(61)
+    for (b, r, c) in [(1, 11, 11), (2, 16, 20), (3, 37, 45), (1, 300, 257), (2, 5, 7)]:
+        a = rng.uniform(0, 255, (b, r, c))
+        y = np.clip(a + rng.normal(0, 15, (b, r, c)), 0, 255)
+        if dtype == torch.float32:
+            a, y = a.astype(np.float32).astype(np.float64), y.astype(np.float32).astype(np.float64)
+        got = host(pl.image_metrics(dev(a, dtype), dev(y, dtype)))
+        for k in range(b):
+            if r < 11 or c < 11:
+                want_mse = float(np.mean((a[k] - y[k]) ** 2))
+                assert abs(got[k, 0] - want_mse) <= 1e-12 * want_mse and np.isnan(got[k, 2])
+                continue
+            want = orc.metrics(a[k], y[k])
+            assert np.allclose(got[k], want, rtol=1e-12, atol=0), (b, r, c, got[k], want)
+    x = dev(rng.uniform(0, 255, (2, 30, 40)), dtype)
+    m = host(pl.image_metrics(x, x))
+    assert (m[:, 0] == 0).all() and np.isinf(m[:, 1]).all() and (m[:, 2] == 1.0).all()
+
+
 def test_guard_bands_no_stray_access():
     """Stand-in for compute-sanitizer (closed on this pool): every kernel path runs on
     inputs/outputs embedded in NaN guard bands.  A stray read poisons an output with

@@ -130,6 +130,21 @@ def test_golden_c1(orc, golden):
     assert np.array_equal(orc.distance_band(f[:4096], S, K), golden["c1_dist_head"], equal_nan=True)
 
 
+def test_golden_metrics(orc, golden):
+    for t, _ in enumerate(golden["metric_cases"]):
+        got = orc.metrics(golden[f"m{t}_a"], golden[f"m{t}_b"])
+        assert np.array_equal(np.array(got), golden[f"m{t}_metrics"]), t
+
+
+def test_metrics_edge_cases(orc):
+    a = np.random.default_rng(3).uniform(0, 255, (12, 15))
+    mse, psnr, ssim = orc.metrics(a, a)
+    assert mse == 0.0 and psnr == float("inf") and ssim == 1.0
+    from oracle import OracleError
+    with pytest.raises(OracleError, match="11x11 structural window"):
+        orc.metrics(a[:10], a[:10])
+
+
 # ---- bit for bit against the reference library -----------------------------
 def test_oracle_equals_reference_1d(orc, ref):
     rng = np.random.default_rng(101)
@@ -166,3 +181,12 @@ def test_oracle_ops_equal_reference(orc, ref):
     orc.nlm_1d(f, 6, 2, 40.0, ops=a)
     ref.nlm_1d(f, 6, 2, 40.0, ops=b)
     assert a == b
+
+
+def test_oracle_metrics_equal_reference(orc, ref):
+    rng = np.random.default_rng(105)
+    for _ in range(6):
+        r, c = int(rng.integers(11, 60)), int(rng.integers(11, 60))
+        a = rng.uniform(0, 255, (r, c))
+        b = np.clip(a + rng.normal(0, 15, (r, c)), 0, 255)
+        assert orc.metrics(a, b) == ref.metrics(a, b)
