@@ -188,11 +188,12 @@ __global__ void direct_pass_kernel(plgpu::PassDesc g) {
   const int blk = g.dst_pos_block;
   float* dst = g.dst + img * g.dst_img_stride + li * g.dst_line_stride +
                (int64_t)(i / blk) * g.dst_block_stride + (int64_t)(i % blk) * g.dst_pos_stride;
-  *dst = fminf(fmaxf(num / den, vmin), vmax);
+  *dst = plgpu::epi(g.avg, g.dst, dst, fminf(fmaxf(num / den, vmin), vmax));
 }
 
 // Production walker launch, if the geometry qualifies (returns -1 if not).
 int try_pass2(const plgpu::PassDesc& g, cudaStream_t st) {
+  if (g.avg && g.src_pos_stride == 1) return -1;  // fused average: column-mode stores only
   // A warp carries 32-64 lines: for a handful of lines the one-thread-per-
   // segment portable walker wastes less.
   if (force_portable() || g.K > 7 || g.S < 1 || g.S > kMaxWalkS || g.lines_per_img < 16) return -1;
@@ -224,6 +225,7 @@ int try_pass2(const plgpu::PassDesc& g, cudaStream_t st) {
   d.K = g.K;
   d.coef = g.coef;
   d.scale = g.scale;
+  d.avg = g.avg;
   const int64_t images = g.n_lines / g.lines_per_img;
   d.total_warps = images * d.groups_per_img * d.nseg;
   const auto a16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
@@ -605,7 +607,7 @@ int pl_nlm_row_pass_blocked(const float* src, float* dst, int32_t batch, int32_t
 
 size_t pl_workspace_bytes(int32_t op, int32_t batch, int32_t rows, int32_t cols) {
   const size_t img = (size_t)std::max(batch, 0) * std::max(rows, 0) * std::max(cols, 0) * sizeof(float);
-  return op == 2 ? 3 * img : img;  // op 2: snlm (RC, CR, mid); else one intermediate
+  return op == 2 ? 2 * img : img;  // op 2: snlm (CR, mid); else one intermediate
 }
 
 int pl_snlm_2d_row_col(const float* src, float* dst, float* work, int32_t batch, int32_t rows,
@@ -643,14 +645,16 @@ int pl_snlm_2d(const float* src, float* dst, float* work, int32_t batch, int32_t
   if (rc) return rc;
   if (!work && (rc = get_workspace(pl_workspace_bytes(2, batch, rows, cols), &work))) return rc;
   const int64_t cnt = (int64_t)batch * rows * cols;
-  float* rc_img = work;
-  float* cr_img = work + cnt;
-  float* mid = work + 2 * cnt;
-  if ((rc = pl_snlm_2d_row_col(src, rc_img, mid, batch, rows, cols, p, stream))) return rc;
+  float* cr_img = work;
+  float* mid = work + cnt;
+  // CR into the workspace, then RC with the average fused into the final
+  // column pass's store: dst = (CR + RC) / 2 (average(), nlm.cpp:106-112).
   if ((rc = pl_snlm_2d_col_row(src, cr_img, mid, batch, rows, cols, p, stream))) return rc;
-  const int blocks = (int)std::min<int64_t>((cnt + 255) / 256, 148 * 16);
-  plgpu::average_kernel<<<blocks, 256, 0, as_stream(stream)>>>(rc_img, cr_img, dst, cnt);
-  return check_launch();
+  cudaStream_t st = as_stream(stream);
+  if ((rc = run_pass(row_desc(src, mid, batch, rows, cols), p, st))) return rc;
+  plgpu::PassDesc g = col_desc(mid, dst, batch, rows, cols);
+  g.avg = cr_img;
+  return run_pass(g, p, st);
 }
 
 int pl_snlm_2d_row_col_host(const float* host_src, float* host_dst, int32_t batch, int32_t rows,

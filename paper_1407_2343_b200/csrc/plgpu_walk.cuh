@@ -60,6 +60,7 @@ struct PassDesc {
   int32_t nseg;     // segments processed (ceil(n / C) unless windowed)
   int32_t seg_begin;  // index of the first processed segment (windowed passes)
   float scale;        // sqrt(log2 e) / h: distance-side sample prescale
+  const float* avg;   // optional, dst layout: store (avg + out) / 2 (snlm_2d's average)
   int32_t S;        // effective search radius, <= template S, <= n-1
   int32_t K;        // patch radius
   float coef;       // -log2(e) / h^2
@@ -69,6 +70,12 @@ __device__ __forceinline__ float ex2_approx(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+}
+
+// Output epilogue: plain store, or the S-NLM average (a + b) / 2 with the
+// other order's result (average(), nlm.cpp:106-112) fused into the store.
+__device__ __forceinline__ float epi(const float* avg, const float* dst, const float* p, float v) {
+  return avg ? (__ldg(avg + (p - dst)) + v) / 2.0f : v;
 }
 
 // num / den for the filter output: one MUFU.RCP and a multiply (within ~2 ulp
@@ -179,7 +186,7 @@ __device__ __forceinline__ void walk_segment(const PassDesc& g, const float* __r
         ad[rk] += w;
       }
       if (i >= s0) {
-        *op = fminf(fmaxf(div_fix(num, den), lo), hi);
+        *op = epi(g.avg, g.dst, op, fminf(fmaxf(div_fix(num, den), lo), hi));
         op += dps;
         if (--orem == 0) {
           op += g.dst_block_stride - (int64_t)blk * dps;

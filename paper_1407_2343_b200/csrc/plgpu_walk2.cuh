@@ -180,6 +180,7 @@ struct Pass2Desc {
   int32_t n, seg_len, nseg, S, K;
   int32_t seg_begin;  // first processed segment (windowed passes; nseg counts from it)
   float scale;        // sqrt(log2 e) / h: distance-side sample prescale
+  const float* avg;   // optional, dst layout (column passes): store (avg + out) / 2
   int32_t vec16;  // column pass: 16-byte copies legal (aligned, full line groups)
   int64_t total_warps;
   float coef;
@@ -387,13 +388,19 @@ __device__ __forceinline__ void walk2(const Pass2Desc& g, float* ring, const int
         } else {
           if constexpr (LINES == 2) {
             if (g.vec16) {
-              *reinterpret_cast<float2*>(op) = make_float2(o0, o1);
+              float2 v = make_float2(o0, o1);
+              if (g.avg) {
+                const float2 a = __ldg(reinterpret_cast<const float2*>(g.avg + (op - g.dst)));
+                v = make_float2((a.x + o0) / 2.0f, (a.y + o1) / 2.0f);
+              }
+              *reinterpret_cast<float2*>(op) = v;
             } else {
-              if (my_line <= last_line) op[0] = o0;
-              if (my_line + 1 <= last_line) op[g.dst_line_stride] = o1;
+              if (my_line <= last_line) op[0] = epi(g.avg, g.dst, op, o0);
+              if (my_line + 1 <= last_line)
+                op[g.dst_line_stride] = epi(g.avg, g.dst, op + g.dst_line_stride, o1);
             }
           } else {
-            if (my_line <= last_line) *op = o0;
+            if (my_line <= last_line) *op = epi(g.avg, g.dst, op, o0);
           }
           op += g.dst_pos_stride;
         }

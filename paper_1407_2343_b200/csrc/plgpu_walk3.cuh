@@ -350,10 +350,16 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
         for (int q = 0; q < R; ++q) {
           const int p = i0 + sb + q;
           if (p >= s0 && p < s1) {
-            if constexpr (LINES == 2)
-              *reinterpret_cast<float2*>(dp) = *reinterpret_cast<const float2*>(sp);
-            else
-              *dp = *sp;
+            if constexpr (LINES == 2) {
+              float2 v = *reinterpret_cast<const float2*>(sp);
+              if (g.avg) {
+                const float2 a = __ldg(reinterpret_cast<const float2*>(g.avg + (dp - g.dst)));
+                v = make_float2((a.x + v.x) / 2.0f, (a.y + v.y) / 2.0f);
+              }
+              *reinterpret_cast<float2*>(dp) = v;
+            } else {
+              *dp = epi(g.avg, g.dst, dp, *sp);
+            }
           }
           dp += g.dst_pos_stride;
           sp += PITCH;
@@ -366,9 +372,14 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
           const int q = qb + lane / LPR;
           const int p = i0 + sb + q;
           if (q < R && p >= s0 && p < s1) {
-            const float4 v = *reinterpret_cast<const float4*>(oring + q * PITCH + 4 * (lane % LPR));
-            *reinterpret_cast<float4*>(g.dst + dst_img + (int64_t)p * g.dst_pos_stride + l0 +
-                                       4 * (lane % LPR)) = v;
+            float4 v = *reinterpret_cast<const float4*>(oring + q * PITCH + 4 * (lane % LPR));
+            const int64_t off = dst_img + (int64_t)p * g.dst_pos_stride + l0 + 4 * (lane % LPR);
+            if (g.avg) {
+              const float4 a = __ldg(reinterpret_cast<const float4*>(g.avg + off));
+              v = make_float4((a.x + v.x) / 2.0f, (a.y + v.y) / 2.0f, (a.z + v.z) / 2.0f,
+                              (a.w + v.w) / 2.0f);
+            }
+            *reinterpret_cast<float4*>(g.dst + off) = v;
           }
         }
         __syncwarp();
@@ -380,9 +391,11 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
           if (p >= s0 && p < s1) {
 #pragma unroll
             for (int h = 0; h < LINES; ++h)
-              if (my_line + h <= last_line)
-                g.dst[dst_img + (int64_t)p * g.dst_pos_stride + (int64_t)(my_line + h) * g.dst_line_stride] =
-                    oring[q * PITCH + lane * LINES + h];
+              if (my_line + h <= last_line) {
+                float* dp = g.dst + dst_img + (int64_t)p * g.dst_pos_stride +
+                            (int64_t)(my_line + h) * g.dst_line_stride;
+                *dp = epi(g.avg, g.dst, dp, oring[q * PITCH + lane * LINES + h]);
+              }
           }
         }
         __syncwarp();

@@ -217,10 +217,15 @@ def test_transpose_equivariance_bitwise():
         assert np.array_equal(host(pl.nlm_col_pass(x, p)), host(pl.nlm_row_pass(xt, p)).T)
 
 
-def test_snlm_is_mean_of_orders_bitwise():
-    img = np.random.default_rng(27).uniform(0, 255, (40, 52)).astype(np.float32)
+@pytest.mark.parametrize("shape,p", [((40, 52), (5, 1, 45.0)), ((2, 300, 256), (10, 3, 60.0)),
+                                     ((1, 130, 128), (15, 5, 90.0)), ((1, 90, 64), (25, 7, 99.0)),
+                                     ((37, 1), (5, 1, 45.0)), ((1, 29), (4, 1, 45.0)),
+                                     ((33, 70), (40, 2, 45.0)), ((3, 20, 24), (6, 9, 45.0))])
+def test_snlm_is_mean_of_orders_bitwise(shape, p):
+    """snlm_2d fuses the average into RC's final column-pass store (every
+    walker and the direct route): bitwise (RC + CR) / 2."""
+    img = np.random.default_rng(27).uniform(0, 255, shape).astype(np.float32)
     x = dev(img)
-    p = (5, 1, 45.0)
     rc = host(pl.snlm_2d_row_col(x, p))
     cr = host(pl.snlm_2d_col_row(x, p))
     assert np.array_equal(host(pl.snlm_2d(x, p)), (rc + cr) / np.float32(2))
