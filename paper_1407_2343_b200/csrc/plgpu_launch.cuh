@@ -83,18 +83,18 @@ bool launch_pass3(const Pass3Desc& d, bool rows, cudaStream_t st) {
         const int64_t images = groups / d.b.groups_per_img;
         const int64_t ctas = images * ((d.b.groups_per_img + 7) / 8) * d.b.nseg;
         const size_t sr = 4 * smem_r, sc = 4 * smem_c;
-        if (rows) {
-          auto k = nlm_pass3_kernel<ST, KT, L, true, 8>;
-          cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sr);
-          k<<<(unsigned)ctas, 256, sr, st>>>(d);
-        } else {
-          auto k = nlm_pass3_kernel<ST, KT, L, false, 8>;
-          cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sc);
-          k<<<(unsigned)ctas, 256, sc, st>>>(d);
-        }
+        auto run = [&](auto k, size_t bytes) {
+          cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+          k<<<(unsigned)ctas, 256, bytes, st>>>(d);
+        };
+        if (rows) run(nlm_pass3_kernel<ST, KT, L, true, 8>, sr);
+        else if (d.b.avg) run(nlm_pass3_kernel<ST, KT, L, false, 8, true>, sc);
+        else run(nlm_pass3_kernel<ST, KT, L, false, 8>, sc);
         return;
       }
       if (rows) nlm_pass3_kernel<ST, KT, L, true><<<blocks, 32 * kWarpsPerCta, smem_r, st>>>(d);
+      else if (d.b.avg)
+        nlm_pass3_kernel<ST, KT, L, false, kWarpsPerCta, true><<<blocks, 32 * kWarpsPerCta, smem_c, st>>>(d);
       else nlm_pass3_kernel<ST, KT, L, false><<<blocks, 32 * kWarpsPerCta, smem_c, st>>>(d);
     };
     if constexpr (ST <= 16) {

@@ -57,7 +57,7 @@ __host__ __device__ constexpr bool pass3_split(int ST) { return ST > 16; }  // S
 // MODE 0: unified (per-chunk mirror check, per-iteration masked/unmasked
 // body).  MODE 1: interior segment only (no mirrored staging, no masked body
 // compiled: smaller code for large S).  MODE 2: edge segment (always masked).
-template <int ST, int KT, int LINES, bool ROWS, int MODE = 0>
+template <int ST, int KT, int LINES, bool ROWS, int MODE = 0, bool AVG = false>
 __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int lane,
                                       const int64_t grp, const int seg, const int bar_threads = 0) {
   using Ops = VecOps<LINES>;
@@ -346,23 +346,33 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
       if (own) {  // each lane stores its own lines: no warp barrier
         float* dp = g.dst + dst_img + (int64_t)(i0 + sb) * g.dst_pos_stride + my_line;
         const float* sp = oring + LINES * lane;
+        if constexpr (AVG) {  // fused S-NLM average: all partner loads before any store
+          const float2* ap = reinterpret_cast<const float2*>(g.avg + (dp - g.dst));
+          float2 a[R];
 #pragma unroll
-        for (int q = 0; q < R; ++q) {
-          const int p = i0 + sb + q;
-          if (p >= s0 && p < s1) {
-            if constexpr (LINES == 2) {
-              float2 v = *reinterpret_cast<const float2*>(sp);
-              if (g.avg) {
-                const float2 a = __ldg(reinterpret_cast<const float2*>(g.avg + (dp - g.dst)));
-                v = make_float2((a.x + v.x) / 2.0f, (a.y + v.y) / 2.0f);
-              }
-              *reinterpret_cast<float2*>(dp) = v;
-            } else {
-              *dp = epi(g.avg, g.dst, dp, *sp);
-            }
+          for (int q = 0; q < R; ++q) {
+            const int p = i0 + sb + q;
+            a[q] = (p >= s0 && p < s1) ? __ldg(ap) : make_float2(0.f, 0.f);
+            ap += g.dst_pos_stride / 2;
           }
-          dp += g.dst_pos_stride;
-          sp += PITCH;
+#pragma unroll
+          for (int q = 0; q < R; ++q) {
+            const int p = i0 + sb + q;
+            if (p >= s0 && p < s1) {
+              const float2 v = *reinterpret_cast<const float2*>(sp);
+              *reinterpret_cast<float2*>(dp) = make_float2((a[q].x + v.x) / 2.0f, (a[q].y + v.y) / 2.0f);
+            }
+            dp += g.dst_pos_stride;
+            sp += PITCH;
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < R; ++q) {
+            const int p = i0 + sb + q;
+            if (p >= s0 && p < s1) *reinterpret_cast<float2*>(dp) = *reinterpret_cast<const float2*>(sp);
+            dp += g.dst_pos_stride;
+            sp += PITCH;
+          }
         }
       } else if (g.vec16) {
         __syncwarp();
@@ -374,7 +384,7 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
           if (q < R && p >= s0 && p < s1) {
             float4 v = *reinterpret_cast<const float4*>(oring + q * PITCH + 4 * (lane % LPR));
             const int64_t off = dst_img + (int64_t)p * g.dst_pos_stride + l0 + 4 * (lane % LPR);
-            if (g.avg) {
+            if constexpr (AVG) {  // fused S-NLM average
               const float4 a = __ldg(reinterpret_cast<const float4*>(g.avg + off));
               v = make_float4((a.x + v.x) / 2.0f, (a.y + v.y) / 2.0f, (a.z + v.z) / 2.0f,
                               (a.w + v.w) / 2.0f);
@@ -394,7 +404,7 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
               if (my_line + h <= last_line) {
                 float* dp = g.dst + dst_img + (int64_t)p * g.dst_pos_stride +
                             (int64_t)(my_line + h) * g.dst_line_stride;
-                *dp = epi(g.avg, g.dst, dp, oring[q * PITCH + lane * LINES + h]);
+                *dp = epi(AVG ? g.avg : nullptr, g.dst, dp, oring[q * PITCH + lane * LINES + h]);
               }
           }
         }
@@ -440,7 +450,7 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
 // WPC = warps per CTA.  WPC = 2: independent warps.  WPC = 8 ("lockstep"):
 // the CTA's warps take 8 consecutive line groups of ONE segment and
 // synchronise once per iteration (named barrier over the active warps).
-template <int ST, int KT, int LINES, bool ROWS, int WPC = kWarpsPerCta>
+template <int ST, int KT, int LINES, bool ROWS, int WPC = kWarpsPerCta, bool AVG = false>
 __global__ void __launch_bounds__(32 * WPC, 1)
     nlm_pass3_kernel(const Pass3Desc d) {
   extern __shared__ __align__(16) float smem[];
@@ -476,30 +486,30 @@ __global__ void __launch_bounds__(32 * WPC, 1)
     const int64_t grp = img * g.groups_per_img + gb + wib;
     const int bt = active * 32;
     if constexpr (!pass3_split(ST)) {
-      walk3<ST, KT, LINES, ROWS, 0>(g, ring, lane, grp, seg, bt);
+      walk3<ST, KT, LINES, ROWS, 0, AVG>(g, ring, lane, grp, seg, bt);
     } else if (interior) {
-      walk3<ST, KT, LINES, ROWS, 1>(g, ring, lane, grp, seg, bt);
+      walk3<ST, KT, LINES, ROWS, 1, AVG>(g, ring, lane, grp, seg, bt);
     } else {
-      walk3<ST, KT, LINES, ROWS, 2>(g, ring, lane, grp, seg, bt);
+      walk3<ST, KT, LINES, ROWS, 2, AVG>(g, ring, lane, grp, seg, bt);
     }
     return;
   }
   const int64_t wid = (int64_t)blockIdx.x * WPC + wib;
   if (wid >= g.total_warps) return;
   if constexpr (!pass3_split(ST)) {
-    walk3<ST, KT, LINES, ROWS, 0>(g, ring, lane, wid / g.nseg, g.seg_begin + (int)(wid % g.nseg));
+    walk3<ST, KT, LINES, ROWS, 0, AVG>(g, ring, lane, wid / g.nseg, g.seg_begin + (int)(wid % g.nseg));
   } else {
     // large S: interior warps (segments needing no clipping) first, then edges
     const int n_int = max(0, d.seg_hi - d.seg_lo + 1);
     if (wid < d.interior_warps) {
-      walk3<ST, KT, LINES, ROWS, 1>(g, ring, lane, wid / n_int,
+      walk3<ST, KT, LINES, ROWS, 1, AVG>(g, ring, lane, wid / n_int,
                                      g.seg_begin + d.seg_lo + (int)(wid % n_int));
     } else {
       const int n_edge = g.nseg - n_int;
       const int64_t e = wid - d.interior_warps;
       int sidx = (int)(e % n_edge);
       if (n_int > 0 && sidx >= d.seg_lo) sidx += n_int;
-      walk3<ST, KT, LINES, ROWS, 2>(g, ring, lane, e / n_edge, g.seg_begin + sidx);
+      walk3<ST, KT, LINES, ROWS, 2, AVG>(g, ring, lane, e / n_edge, g.seg_begin + sidx);
     }
   }
 }
