@@ -200,9 +200,92 @@ __global__ void pk_kernel(float* out, int iters) {
   if (s == 1.2345f) out[threadIdx.x] = s;
 }
 
+// Mixed-pipe issue test: per iteration NF2 independent FFMA2, NF1 scalar
+// FFMA, NMU MUFU.EX2 (8 rotating chains) and NAL integer ALU ops.  Comparing
+// the mixes tells whether FFMA2 and MUFU share the dispatch port (times add)
+// or overlap (time = max).
+template <int NF2, int NF1, int NMU, int NAL>
+__global__ void mix_kernel(float* out, int iters) {
+  using O = plgpu::VecOps<2>;
+  using V = O::V;
+  V x[8], y[8];
+  float xs[16], m[8];
+  int xi[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    x[k] = plgpu::f2_make(threadIdx.x * 1e-3f + k, k * 0.5f);
+    y[k] = plgpu::f2_make(0.999f - k * 1e-4f, 1.0001f + k * 1e-5f);
+    m[k] = -0.5f - k * 0.01f;
+    xi[k] = threadIdx.x * 7 + k;
+  }
+#pragma unroll
+  for (int k = 0; k < 16; ++k) xs[k] = threadIdx.x * 1e-3f + k;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int k = 0; k < (NF2 > 8 ? 8 : NF2); ++k) x[k] = O::fma(x[k], y[k], x[(k + 3) % 8]);
+#pragma unroll
+    for (int k = 8; k < NF2; ++k) x[k - 8] = O::fma(x[k - 8], y[k - 8], x[(k + 1) % 8]);
+#pragma unroll
+    for (int k = 0; k < NF1; ++k) xs[k % 16] = fmaf(xs[k % 16], 0.999f, xs[(k + 5) % 16]);
+#pragma unroll
+    for (int k = 0; k < NMU; ++k) {
+      const int j = (it * NMU + k) & 7;
+      m[j] = -plgpu::ex2_approx(m[j]);
+    }
+#pragma unroll
+    for (int k = 0; k < NAL; ++k) xi[k & 7] = xi[k & 7] + xi[(k + 3) & 7];
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += O::lo(x[k]) + O::hi(x[k]) + m[k] + (float)xi[k];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) s += xs[k];
+  if (s == 1.2345f) out[threadIdx.x] = s;
+}
+
 }  // namespace
 
 extern "C" {
+
+// Cycles per loop iteration per SM sub-partition (at the given clock in MHz)
+// for mix_kernel preset `which`; -1 on error.
+double plub_mix_cycles(int which, int blocks_per_sm, int threads, int iters, double mhz) {
+  int dev = 0, sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  float* out = nullptr;
+  if (cudaMalloc(&out, 4096 * sizeof(float)) != cudaSuccess) return -1;
+  const int blocks = sms * blocks_per_sm;
+  auto launch = [&]() {
+    switch (which) {
+      case 0: mix_kernel<8, 0, 0, 0><<<blocks, threads>>>(out, iters); break;
+      case 1: mix_kernel<0, 0, 2, 0><<<blocks, threads>>>(out, iters); break;
+      case 2: mix_kernel<8, 0, 2, 0><<<blocks, threads>>>(out, iters); break;
+      case 3: mix_kernel<0, 16, 0, 0><<<blocks, threads>>>(out, iters); break;
+      case 4: mix_kernel<0, 16, 2, 0><<<blocks, threads>>>(out, iters); break;
+      case 5: mix_kernel<8, 0, 0, 8><<<blocks, threads>>>(out, iters); break;
+      case 6: mix_kernel<0, 0, 0, 8><<<blocks, threads>>>(out, iters); break;
+      case 7: mix_kernel<12, 0, 2, 0><<<blocks, threads>>>(out, iters); break;
+      default: mix_kernel<6, 0, 2, 0><<<blocks, threads>>>(out, iters); break;
+    }
+  };
+  launch();
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  for (int r = 0; r < 3; ++r) launch();
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaFree(out);
+  if (cudaGetLastError() != cudaSuccess) return -1;
+  // warps per SMSP = blocks_per_sm * threads / 32 / 4; each runs iters iterations
+  const double warp_iters_per_smsp = 3.0 * iters * blocks_per_sm * (threads / 32) / 4.0;
+  return (ms * 1e-3) * mhz * 1e6 / warp_iters_per_smsp;
+}
+
 
 // Warp-instructions per second per SM for pk_kernel<op>.
 double plub_pk_rate(int op, int blocks_per_sm, int threads, int iters) {

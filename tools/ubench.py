@@ -29,3 +29,14 @@ for op, name in enumerate(["ffma2_3pair", "fadd2_2pair", "fmul2_2pair", "ffma2_f
         r = L.plub_pk_rate(op, bps, thr, 4000)
         pk[f"{name}_w{bps*thr//32}"] = {"warp_instr_per_clk_per_sm": r / clk, "cycles_per_instr_per_smsp": 4 * clk / r}
 print(json.dumps(pk, indent=1))
+
+# Mixed-pipe dispatch test (cycles per warp-iteration per SMSP).
+L.plub_mix_cycles.restype = C.c_double
+L.plub_mix_cycles.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_double]
+names = ["8xFFMA2", "2xMUFU", "8xFFMA2+2xMUFU", "16xFFMA", "16xFFMA+2xMUFU", "8xFFMA2+8xIADD",
+         "8xIADD", "12xFFMA2+2xMUFU", "6xFFMA2+2xMUFU"]
+mix = {}
+for w, nm in enumerate(names):
+    for bps, thr in ((1, 128), (2, 128), (4, 128)):
+        mix[f"{nm}_warps{bps * thr // 128}"] = round(L.plub_mix_cycles(w, bps, thr, 20000, 1965.0), 2)
+print(json.dumps(mix, indent=1))
