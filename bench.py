@@ -332,8 +332,9 @@ def run_ours(args):
             if p2p:
                 for req in torch.distributed.batch_isend_irecv(p2p):
                     req.wait()
-        else:
-            pl.nlm_row_pass(x, params, out=mid)
+        else:  # row pass into the transposed intermediate (what pl_snlm_2d_row_col runs)
+            R_, C_ = c["rows"], c["cols"]
+            pl.nlm_pass_strided(x, mid, x.shape[0], R_, C_, C_, 1, 1, R_, R_ * C_, params)
 
     def second_pass():
         if signal:
@@ -342,8 +343,9 @@ def run_ours(args):
             pl.nlm_col_pass(recv.reshape(c["rows"], cb), params, out=y)
         elif halo:
             pl.nlm_col_pass_window(win, wlo, c["rows"], seg_a, seg_b, params, out=y)
-        else:
-            pl.nlm_col_pass(mid, params, out=y)
+        else:  # column pass reading the transposed intermediate
+            R_, C_ = c["rows"], c["cols"]
+            pl.nlm_pass_strided(mid, y, x.shape[0], C_, R_, R_, 1, 1, C_, R_ * C_, params)
 
     def step():
         first_pass()

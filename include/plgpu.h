@@ -128,6 +128,16 @@ int pl_nlm_col_pass_window(const float* src, int32_t in_lo, int32_t in_rows, flo
                            int32_t batch, int32_t rows_total, int32_t cols, int32_t seg_begin,
                            int32_t seg_end, pl_params p, void* stream);
 
+/* One pass over `lines` lines of n samples per image, any layout:
+ * element (b, line, pos) of src at b*img_stride + line*src_line_stride +
+ * pos*src_pos_stride, of dst likewise with the dst strides.  Row pass:
+ * (cols, 1, cols, 1); column pass: (1, cols, 1, cols); the RC composite's
+ * transposed intermediate: row pass (cols, 1, 1, rows) then column pass
+ * (rows, 1, 1, cols) -- what pl_snlm_2d_row_col runs internally. */
+int pl_nlm_pass_strided(const float* src, float* dst, int32_t batch, int32_t lines, int32_t n,
+                        int64_t src_line_stride, int64_t src_pos_stride, int64_t dst_line_stride,
+                        int64_t dst_pos_stride, int64_t img_stride, pl_params p, void* stream);
+
 /* Row pass whose output is written in column blocks of width col_block:
  * element (b, r, c) lands at dst + b*rows*cols + (c / col_block)*rows*col_block
  * + r*col_block + (c % col_block).  With one image per rank this is exactly

@@ -36,6 +36,7 @@ EXPORTS = [
     "pl_device_alloc", "pl_device_free", "pl_copy_to_device", "pl_copy_to_host",
     "pl_synchronize", "pl_distance_band_f32", "pl_distance_band_i32", "pl_banded_kernel_f64",
     "pl_col_window", "pl_nlm_col_pass_window", "pl_image_metrics_f32", "pl_image_metrics_f64",
+    "pl_nlm_pass_strided",
 ]
 
 
@@ -96,6 +97,8 @@ def lib() -> C.CDLL:
             "pl_nlm_row_pass_blocked": ([vp, vp, i32, i32, i32, i32, P, vp], C.c_int),
             "pl_col_window": ([i32, i32, i32, P] + [C.POINTER(i32)] * 4, C.c_int),
             "pl_image_metrics_f32": ([vp, vp, i32, i32, i32, vp, vp], C.c_int),
+            "pl_nlm_pass_strided": ([vp, vp, i32, i32, i32, i64, i64, i64, i64, i64, P, vp],
+                                    C.c_int),
             "pl_image_metrics_f64": ([vp, vp, i32, i32, i32, vp, vp], C.c_int),
             "pl_nlm_col_pass_window": ([vp, i32, i32, vp, i32, i32, i32, i32, i32, P, vp],
                                        C.c_int),
@@ -293,6 +296,20 @@ def nlm_col_pass_window(x_win, in_lo: int, rows_total: int, seg_begin: int, seg_
                                         int(rows_total), c, int(seg_begin), int(seg_end),
                                         _params(p), _stream(x_win)))
     return out
+
+
+def nlm_pass_strided(src, dst, batch: int, lines: int, n: int, src_line_stride: int,
+                     src_pos_stride: int, dst_line_stride: int, dst_pos_stride: int,
+                     img_stride: int, p):
+    """One pass over arbitrarily strided lines of device tensors (see plgpu.h)."""
+    import torch
+    _dev(src, torch.float32)
+    _dev(dst, torch.float32)
+    _check(lib().pl_nlm_pass_strided(src.data_ptr(), dst.data_ptr(), int(batch), int(lines), int(n),
+                                     int(src_line_stride), int(src_pos_stride),
+                                     int(dst_line_stride), int(dst_pos_stride), int(img_stride),
+                                     _params(p), _stream(src)))
+    return dst
 
 
 def workspace_bytes(op: int, batch: int, rows: int, cols: int) -> int:

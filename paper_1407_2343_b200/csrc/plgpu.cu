@@ -201,7 +201,11 @@ int try_pass2(const plgpu::PassDesc& g, cudaStream_t st) {
   const int LW = 32 * plgpu::pass2_lines(ST);
   const bool rows = g.src_pos_stride == 1 && g.dst_pos_stride == 1;
   const bool cols = g.src_line_stride == 1 && g.dst_line_stride == 1;
-  if (!rows && !cols) return -1;
+  // positions contiguous in the source, lines contiguous in the destination:
+  // the transposed-intermediate RC composite (walk3 io = 2; walk2 treats it
+  // as a column pass with general source strides)
+  const bool mixed = !rows && g.src_pos_stride == 1 && g.dst_line_stride == 1;
+  if (!rows && !cols && !mixed) return -1;
   if (rows && g.dst_pos_block != g.n && g.dst_pos_block % plgpu::kCH != 0) return -1;
   if (!rows && g.dst_pos_block != g.n) return -1;
   plgpu::Pass2Desc d{};
@@ -246,9 +250,13 @@ int try_pass2(const plgpu::PassDesc& g, cudaStream_t st) {
       const int LW3 = 32 * d3.lines;
       d3.b.groups_per_img = (g.lines_per_img + LW3 - 1) / LW3;
       d3.b.total_warps = images * d3.b.groups_per_img * d.nseg;
-      d3.b.vec16 = !rows && g.lines_per_img % LW3 == 0 && g.src_pos_stride % 4 == 0 &&
-                   g.src_img_stride % 4 == 0 && g.dst_pos_stride % 4 == 0 &&
-                   g.dst_img_stride % 4 == 0 && a16(g.src) && a16(g.dst);
+      const int io = rows ? 1 : (mixed ? 2 : 0);
+      const bool dst16 = g.lines_per_img % LW3 == 0 && g.dst_line_stride == 1 &&
+                         g.dst_pos_stride % 4 == 0 && g.dst_img_stride % 4 == 0 && a16(g.dst);
+      const bool src16 = g.src_line_stride == 1 && g.src_pos_stride % 4 == 0 &&
+                         g.src_img_stride % 4 == 0 && a16(g.src);
+      // io 0: 16-byte staging copies and stores; io 2: 16-byte stores only
+      d3.b.vec16 = io == 0 ? (dst16 && src16) : io == 2 ? dst16 : false;
       int lo = d.nseg, hi = -1;
       for (int sgi = 0; sgi < d.nseg; ++sgi) {
         const int s0 = (d.seg_begin + sgi) * d.seg_len, s1 = std::min(d.n, s0 + d.seg_len);
@@ -272,7 +280,7 @@ int try_pass2(const plgpu::PassDesc& g, cudaStream_t st) {
       bool launched = false;
       switch (ST) {
 #define PL_CASE(v) \
-  case v: launched = plgpu::launch_pass3<v>(d3, rows, st); break;
+  case v: launched = plgpu::launch_pass3<v>(d3, io, st); break;
         PLGPU_FOR_EACH_RADIUS(PL_CASE)
 #undef PL_CASE
       }
@@ -340,6 +348,26 @@ plgpu::PassDesc col_desc(const float* src, float* dst, int batch, int rows, int 
   g.dst_pos_block = rows;
   g.n = rows;
   return g;
+}
+
+// Row -> column composite with a TRANSPOSED intermediate: the row pass
+// stores its lines as columns of `mid` ([cols][rows] per image), so both
+// passes stage positions along contiguous memory and flush lines along
+// contiguous memory (walk3 io = 2), instead of the row pass paying a
+// transposing flush.  Same per-line arithmetic: bit-identical to the
+// row_desc/col_desc pair.  `avg` (optional) fuses the S-NLM average.
+int rc_passes(const float* src, float* dst, float* mid, int batch, int rows, int cols,
+              const pl_params& p, cudaStream_t st, const float* avg = nullptr) {
+  plgpu::PassDesc a = row_desc(src, mid, batch, rows, cols);
+  a.dst_line_stride = 1;
+  a.dst_pos_stride = rows;
+  int rc = run_pass(a, p, st);
+  if (rc) return rc;
+  plgpu::PassDesc b = col_desc(mid, dst, batch, rows, cols);
+  b.src_line_stride = rows;
+  b.src_pos_stride = 1;
+  b.avg = avg;
+  return run_pass(b, p, st);
 }
 
 // Library-owned workspace cache (per device, grown on demand, stream-ordered use).
@@ -590,6 +618,31 @@ int pl_nlm_col_pass_window(const float* src, int32_t in_lo, int32_t in_rows, flo
   return run_pass(g, p, as_stream(stream));
 }
 
+int pl_nlm_pass_strided(const float* src, float* dst, int32_t batch, int32_t lines, int32_t n,
+                        int64_t src_line_stride, int64_t src_pos_stride, int64_t dst_line_stride,
+                        int64_t dst_pos_stride, int64_t img_stride, pl_params p, void* stream) {
+  int rc = validate_image(batch, lines, n);
+  if (!rc) rc = validate_params(p, n);
+  if (!rc) rc = check_ptrs(src, dst);
+  if (rc) return rc;
+  if (src_line_stride < 0 || src_pos_stride < 1 || dst_line_stride < 0 || dst_pos_stride < 1 ||
+      img_stride < 0)
+    return set_err(PL_ERR_ARG, "strides must be nonnegative (position strides positive)");
+  plgpu::PassDesc g{};
+  g.src = src;
+  g.dst = dst;
+  g.n_lines = (int64_t)batch * lines;
+  g.lines_per_img = lines;
+  g.src_img_stride = g.dst_img_stride = img_stride;
+  g.src_line_stride = src_line_stride;
+  g.src_pos_stride = src_pos_stride;
+  g.dst_line_stride = dst_line_stride;
+  g.dst_pos_stride = dst_pos_stride;
+  g.dst_pos_block = n;
+  g.n = n;
+  return run_pass(g, p, as_stream(stream));
+}
+
 int pl_nlm_row_pass_blocked(const float* src, float* dst, int32_t batch, int32_t rows,
                             int32_t cols, int32_t col_block, pl_params p, void* stream) {
   int rc = validate_image(batch, rows, cols);
@@ -618,9 +671,7 @@ int pl_snlm_2d_row_col(const float* src, float* dst, float* work, int32_t batch,
   if (!rc) rc = check_ptrs(src, dst);
   if (rc) return rc;
   if (!work && (rc = get_workspace(pl_workspace_bytes(0, batch, rows, cols), &work))) return rc;
-  cudaStream_t st = as_stream(stream);
-  if ((rc = run_pass(row_desc(src, work, batch, rows, cols), p, st))) return rc;
-  return run_pass(col_desc(work, dst, batch, rows, cols), p, st);
+  return rc_passes(src, dst, work, batch, rows, cols, p, as_stream(stream));
 }
 
 int pl_snlm_2d_col_row(const float* src, float* dst, float* work, int32_t batch, int32_t rows,
@@ -650,11 +701,7 @@ int pl_snlm_2d(const float* src, float* dst, float* work, int32_t batch, int32_t
   // CR into the workspace, then RC with the average fused into the final
   // column pass's store: dst = (CR + RC) / 2 (average(), nlm.cpp:106-112).
   if ((rc = pl_snlm_2d_col_row(src, cr_img, mid, batch, rows, cols, p, stream))) return rc;
-  cudaStream_t st = as_stream(stream);
-  if ((rc = run_pass(row_desc(src, mid, batch, rows, cols), p, st))) return rc;
-  plgpu::PassDesc g = col_desc(mid, dst, batch, rows, cols);
-  g.avg = cr_img;
-  return run_pass(g, p, st);
+  return rc_passes(src, dst, mid, batch, rows, cols, p, as_stream(stream), cr_img);
 }
 
 int pl_snlm_2d_row_col_host(const float* host_src, float* host_dst, int32_t batch, int32_t rows,
@@ -702,8 +749,7 @@ int pl_snlm_2d_row_col_host(const float* host_src, float* host_dst, int32_t batc
                     cudaMemcpyHostToDevice, s_in);
     cudaEventRecord(up[k], s_in);
     cudaStreamWaitEvent(st, up[k], 0);
-    if ((rc = run_pass(row_desc(in, mid, nb, rows, cols), p, st))) break;
-    if ((rc = run_pass(col_desc(mid, out, nb, rows, cols), p, st))) break;
+    if ((rc = rc_passes(in, out, mid, nb, rows, cols, p, st))) break;
     cudaEventRecord(done[k], st);
     cudaStreamWaitEvent(s_out, done[k], 0);
     cudaMemcpyAsync(host_dst + (size_t)b0 * img, out, nb * img * sizeof(float),

@@ -28,9 +28,13 @@ constexpr int pass2_lines(int ST) { return ST <= 16 ? 2 : 1; }
 
 // Hot-configuration kernel (plgpu_walk3.cuh) for the (K, S) pairs of the
 // configs; returns false if (g.K, ST) has no instantiation.
+// io: 0 column staging + column flush, 1 row + row, 2 row staging + column
+// flush (plgpu_walk3.cuh).
 template <int ST>
-bool launch_pass3(const Pass3Desc& d, bool rows, cudaStream_t st);
+bool launch_pass3(const Pass3Desc& d, int io, cudaStream_t st);
 constexpr int pass3_k_for(int ST) { return ST == 10 ? 3 : ST == 15 ? 5 : ST == 25 ? 7 : -1; }
+// warps per CTA the configs run with (PLGPU_WPC can override for io 0/1)
+constexpr int pass3_default_wpc(int ST) { return ST >= 15 ? 8 : 2; }
 
 #ifdef PLGPU_DEFINE_LAUNCHERS
 template <int ST>
@@ -65,37 +69,46 @@ void launch_pass2(const Pass2Desc& g, bool rows, cudaStream_t st) {
   launch_pass2_k<ST, -1>(g, rows, st);  // runtime K (K <= 7)
 }
 
+template <int ST, int KT, int L, int IO, int WPC, bool AVG>
+void launch3(const Pass3Desc& d, cudaStream_t st) {
+  const size_t smem = sizeof(float) * WPC * pass3_smem_floats_per_warp<ST, L, IO != 0>();
+  unsigned grid;
+  if constexpr (WPC == 8) {  // 8 line groups of one segment per CTA
+    const int64_t groups = d.b.total_warps / d.b.nseg;
+    const int64_t images = groups / d.b.groups_per_img;
+    grid = (unsigned)(images * ((d.b.groups_per_img + 7) / 8) * d.b.nseg);
+  } else {
+    grid = (unsigned)((d.b.total_warps + WPC - 1) / WPC);
+  }
+  auto k = nlm_pass3_kernel<ST, KT, L, IO, WPC, AVG>;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k<<<grid, 32 * WPC, smem, st>>>(d);
+}
+
 template <int ST>
-bool launch_pass3(const Pass3Desc& d, bool rows, cudaStream_t st) {
+bool launch_pass3(const Pass3Desc& d, int io, cudaStream_t st) {
   constexpr int KT = pass3_k_for(ST);
   if constexpr (KT < 0) {
     return false;
   } else {
     if (d.b.K != KT || d.b.S != ST) return false;
-    const unsigned blocks = (unsigned)((d.b.total_warps + kWarpsPerCta - 1) / kWarpsPerCta);
+    constexpr int DW = pass3_default_wpc(ST);
+    // (register-capped variants, minb 6/8, measured slower on B200: profiles/README.md)
     auto go = [&](auto lines_tag) {
       constexpr int L = decltype(lines_tag)::value;
-      const size_t smem_r = sizeof(float) * kWarpsPerCta * pass3_smem_floats_per_warp<ST, L, true>();
-      const size_t smem_c = sizeof(float) * kWarpsPerCta * pass3_smem_floats_per_warp<ST, L, false>();
-      // (register-capped variants, minb 6/8, measured slower on B200: profiles/README.md)
-      if (d.wpc == 8) {
-        const int64_t groups = d.b.total_warps / d.b.nseg;
-        const int64_t images = groups / d.b.groups_per_img;
-        const int64_t ctas = images * ((d.b.groups_per_img + 7) / 8) * d.b.nseg;
-        const size_t sr = 4 * smem_r, sc = 4 * smem_c;
-        auto run = [&](auto k, size_t bytes) {
-          cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-          k<<<(unsigned)ctas, 256, bytes, st>>>(d);
-        };
-        if (rows) run(nlm_pass3_kernel<ST, KT, L, true, 8>, sr);
-        else if (d.b.avg) run(nlm_pass3_kernel<ST, KT, L, false, 8, true>, sc);
-        else run(nlm_pass3_kernel<ST, KT, L, false, 8>, sc);
-        return;
+      if (io == 1) {
+        if (d.wpc == 8) launch3<ST, KT, L, 1, 8, false>(d, st);
+        else launch3<ST, KT, L, 1, 2, false>(d, st);
+      } else if (io == 0 && !d.b.avg) {
+        if (d.wpc == 8) launch3<ST, KT, L, 0, 8, false>(d, st);
+        else launch3<ST, KT, L, 0, 2, false>(d, st);
+      } else if (io == 0) {
+        launch3<ST, KT, L, 0, DW, true>(d, st);
+      } else if (d.b.avg) {
+        launch3<ST, KT, L, 2, DW, true>(d, st);
+      } else {
+        launch3<ST, KT, L, 2, DW, false>(d, st);
       }
-      if (rows) nlm_pass3_kernel<ST, KT, L, true><<<blocks, 32 * kWarpsPerCta, smem_r, st>>>(d);
-      else if (d.b.avg)
-        nlm_pass3_kernel<ST, KT, L, false, kWarpsPerCta, true><<<blocks, 32 * kWarpsPerCta, smem_c, st>>>(d);
-      else nlm_pass3_kernel<ST, KT, L, false><<<blocks, 32 * kWarpsPerCta, smem_c, st>>>(d);
     };
     if constexpr (ST <= 16) {
       if (d.lines == 2) go(std::integral_constant<int, 2>{});
@@ -108,7 +121,7 @@ bool launch_pass3(const Pass3Desc& d, bool rows, cudaStream_t st) {
 }
 
 #define PLGPU_INSTANTIATE(ST)                                              \
-  template bool launch_pass3<ST>(const Pass3Desc&, bool, cudaStream_t);    \
+  template bool launch_pass3<ST>(const Pass3Desc&, int, cudaStream_t);     \
   template void launch_pass<ST>(const PassDesc&, cudaStream_t);            \
   template void launch_pass2<ST>(const Pass2Desc&, bool, cudaStream_t);    \
   template void launch_band<ST, float>(const BandDesc&, cudaStream_t);     \

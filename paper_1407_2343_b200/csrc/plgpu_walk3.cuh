@@ -57,9 +57,15 @@ __host__ __device__ constexpr bool pass3_split(int ST) { return ST > 16; }  // S
 // MODE 0: unified (per-chunk mirror check, per-iteration masked/unmasked
 // body).  MODE 1: interior segment only (no mirrored staging, no masked body
 // compiled: smaller code for large S).  MODE 2: edge segment (always masked).
-template <int ST, int KT, int LINES, bool ROWS, int MODE = 0, bool AVG = false>
+// IO: 0 = column staging + column flush (lines contiguous on both sides);
+// 1 = row staging + row flush (positions contiguous on both sides);
+// 2 = row staging + column flush (positions contiguous in the source, lines
+// contiguous in the destination: the transposed-intermediate RC composite).
+template <int ST, int KT, int LINES, int IO, int MODE = 0, bool AVG = false>
 __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int lane,
                                       const int64_t grp, const int seg, const int bar_threads = 0) {
+  constexpr bool ROWS = IO != 0;   // transposing (row-mode) staging
+  constexpr bool OROWS = IO == 1;  // row-mode output flush
   using Ops = VecOps<LINES>;
   using V = typename Ops::V;
   constexpr int LW = 32 * LINES;
@@ -71,6 +77,9 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
   static_assert(2 * KT + 2 <= R, "iteration must read at most two chunks");
   static_assert(M <= 2, "prologue must fit the ring");
   float* oring = ring + kNS3 * CHUNK;
+  // output ring pitch: padded (conflict-free transposed reads) only for the
+  // row-mode flush; the column flushes read whole 16-byte rows
+  constexpr int OPITCH = OROWS ? PITCH : LW;
 
   const int64_t img = grp / g.groups_per_img;
   const int l0 = (int)(grp % g.groups_per_img) * LW;
@@ -88,6 +97,8 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
   // Column pass with 2 lines per lane: every lane stages (8-byte copies) and
   // flushes exactly the lines it computes -> no warp barriers around the ring.
   const bool own = !ROWS && LINES == 2 && g.vec16;
+  // column-mode flush where each lane stores exactly the lines it computed
+  const bool oown = !OROWS && LINES == 2 && g.vec16;
 
   auto slot = [&](int c) -> float* { return ring + (c & (kNS3 - 1)) * CHUNK; };
   // Copy chunk c (positions u = cR + BASE + q, q < R); always commits a group.
@@ -103,7 +114,13 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
       const int ubase = c * R + BASE;
       const int pfirst = pos0 + ubase;
       const bool inside = MODE == 1 || (MODE == 0 && pfirst >= 0 && pfirst + R - 1 <= n - 1);
-      if constexpr (ROWS) {
+#ifndef PLGPU_ABL_ROWSTAGE
+#define PLGPU_ABL_ROWSTAGE 0
+#endif
+      if constexpr (ROWS && PLGPU_ABL_ROWSTAGE) {
+        // ablation: stage only the first position row (timing experiment, wrong output)
+        if (lane < 16 && ubase >= 0) cp_async4(dstc + 2 * lane, rows_base + pfirst);
+      } else if constexpr (ROWS) {
 #pragma unroll
         for (int qb = 0; qb < R; qb += 16) {
           const int q = qb + lane16;
@@ -315,7 +332,7 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
         float o1 = o0;
         if constexpr (LINES == 2) o1 = fminf(fmaxf(Ops::hi(qv), lo1), hi1);
         {  // every step lands in the output ring, filtered at the flush
-          float* sl = oring + r * PITCH + lane * LINES;
+          float* sl = oring + r * OPITCH + lane * LINES;
           if constexpr (LINES == 2) *reinterpret_cast<float2*>(sl) = make_float2(o0, o1);
           else *sl = o0;
         }
@@ -341,9 +358,9 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
       else body(std::integral_constant<bool, true>{});
     }
 
-    if constexpr (!ROWS) {
+    if constexpr (!OROWS) {
       // flush this iteration's outputs (row q = position i0 + sb + q)
-      if (own) {  // each lane stores its own lines: no warp barrier
+      if (oown) {  // each lane stores its own lines: no warp barrier
         float* dp = g.dst + dst_img + (int64_t)(i0 + sb) * g.dst_pos_stride + my_line;
         const float* sp = oring + LINES * lane;
         if constexpr (AVG) {  // fused S-NLM average: all partner loads before any store
@@ -363,7 +380,7 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
               *reinterpret_cast<float2*>(dp) = make_float2((a[q].x + v.x) / 2.0f, (a[q].y + v.y) / 2.0f);
             }
             dp += g.dst_pos_stride;
-            sp += PITCH;
+            sp += OPITCH;
           }
         } else {
 #pragma unroll
@@ -371,7 +388,7 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
             const int p = i0 + sb + q;
             if (p >= s0 && p < s1) *reinterpret_cast<float2*>(dp) = *reinterpret_cast<const float2*>(sp);
             dp += g.dst_pos_stride;
-            sp += PITCH;
+            sp += OPITCH;
           }
         }
       } else if (g.vec16) {
@@ -382,7 +399,7 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
           const int q = qb + lane / LPR;
           const int p = i0 + sb + q;
           if (q < R && p >= s0 && p < s1) {
-            float4 v = *reinterpret_cast<const float4*>(oring + q * PITCH + 4 * (lane % LPR));
+            float4 v = *reinterpret_cast<const float4*>(oring + q * OPITCH + 4 * (lane % LPR));
             const int64_t off = dst_img + (int64_t)p * g.dst_pos_stride + l0 + 4 * (lane % LPR);
             if constexpr (AVG) {  // fused S-NLM average
               const float4 a = __ldg(reinterpret_cast<const float4*>(g.avg + off));
@@ -404,14 +421,17 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
               if (my_line + h <= last_line) {
                 float* dp = g.dst + dst_img + (int64_t)p * g.dst_pos_stride +
                             (int64_t)(my_line + h) * g.dst_line_stride;
-                *dp = epi(AVG ? g.avg : nullptr, g.dst, dp, oring[q * PITCH + lane * LINES + h]);
+                *dp = epi(AVG ? g.avg : nullptr, g.dst, dp, oring[q * OPITCH + lane * LINES + h]);
               }
           }
         }
         __syncwarp();
       }
     }
-    if constexpr (ROWS) {
+#ifndef PLGPU_ABL_ROWFLUSH
+#define PLGPU_ABL_ROWFLUSH 0
+#endif
+    if constexpr (OROWS && !PLGPU_ABL_ROWFLUSH) {
       // flush this iteration's outputs: positions p = i0 + sb + q, q < R
       __syncwarp();
 #pragma unroll
@@ -450,14 +470,14 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
 // WPC = warps per CTA.  WPC = 2: independent warps.  WPC = 8 ("lockstep"):
 // the CTA's warps take 8 consecutive line groups of ONE segment and
 // synchronise once per iteration (named barrier over the active warps).
-template <int ST, int KT, int LINES, bool ROWS, int WPC = kWarpsPerCta, bool AVG = false>
+template <int ST, int KT, int LINES, int IO, int WPC = kWarpsPerCta, bool AVG = false>
 __global__ void __launch_bounds__(32 * WPC, 1)
     nlm_pass3_kernel(const Pass3Desc d) {
   extern __shared__ __align__(16) float smem[];
   const Pass2Desc& g = d.b;
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
-  float* ring = smem + wib * pass3_smem_floats_per_warp<ST, LINES, ROWS>();
+  float* ring = smem + wib * pass3_smem_floats_per_warp<ST, LINES, IO != 0>();
   if constexpr (WPC == 8) {
     const int bpi = (g.groups_per_img + 7) / 8;  // 8-group blocks per image
     const int64_t blocks_per_seg = (g.total_warps / g.nseg + 0) / g.groups_per_img * bpi;
@@ -486,30 +506,30 @@ __global__ void __launch_bounds__(32 * WPC, 1)
     const int64_t grp = img * g.groups_per_img + gb + wib;
     const int bt = active * 32;
     if constexpr (!pass3_split(ST)) {
-      walk3<ST, KT, LINES, ROWS, 0, AVG>(g, ring, lane, grp, seg, bt);
+      walk3<ST, KT, LINES, IO, 0, AVG>(g, ring, lane, grp, seg, bt);
     } else if (interior) {
-      walk3<ST, KT, LINES, ROWS, 1, AVG>(g, ring, lane, grp, seg, bt);
+      walk3<ST, KT, LINES, IO, 1, AVG>(g, ring, lane, grp, seg, bt);
     } else {
-      walk3<ST, KT, LINES, ROWS, 2, AVG>(g, ring, lane, grp, seg, bt);
+      walk3<ST, KT, LINES, IO, 2, AVG>(g, ring, lane, grp, seg, bt);
     }
     return;
   }
   const int64_t wid = (int64_t)blockIdx.x * WPC + wib;
   if (wid >= g.total_warps) return;
   if constexpr (!pass3_split(ST)) {
-    walk3<ST, KT, LINES, ROWS, 0, AVG>(g, ring, lane, wid / g.nseg, g.seg_begin + (int)(wid % g.nseg));
+    walk3<ST, KT, LINES, IO, 0, AVG>(g, ring, lane, wid / g.nseg, g.seg_begin + (int)(wid % g.nseg));
   } else {
     // large S: interior warps (segments needing no clipping) first, then edges
     const int n_int = max(0, d.seg_hi - d.seg_lo + 1);
     if (wid < d.interior_warps) {
-      walk3<ST, KT, LINES, ROWS, 1, AVG>(g, ring, lane, wid / n_int,
+      walk3<ST, KT, LINES, IO, 1, AVG>(g, ring, lane, wid / n_int,
                                      g.seg_begin + d.seg_lo + (int)(wid % n_int));
     } else {
       const int n_edge = g.nseg - n_int;
       const int64_t e = wid - d.interior_warps;
       int sidx = (int)(e % n_edge);
       if (n_int > 0 && sidx >= d.seg_lo) sidx += n_int;
-      walk3<ST, KT, LINES, ROWS, 2, AVG>(g, ring, lane, e / n_edge, g.seg_begin + sidx);
+      walk3<ST, KT, LINES, IO, 2, AVG>(g, ring, lane, e / n_edge, g.seg_begin + sidx);
     }
   }
 }

@@ -492,6 +492,30 @@ def test_image_metrics_vs_oracle(dtype):
     assert (m[:, 0] == 0).all() and np.isinf(m[:, 1]).all() and (m[:, 2] == 1.0).all()
 
 
+@pytest.mark.parametrize("shape,p", [((3, 300, 256), (10, 3, 60.0)), ((1, 200, 130), (15, 5, 90.0)),
+                                     ((1, 96, 64), (25, 7, 99.0)), ((2, 70, 90), (4, 2, 50.0)),
+                                     ((1, 33, 20), (6, 9, 45.0)), ((1, 40, 7), (40, 1, 45.0))])
+def test_transposed_intermediate_bitwise(shape, p):
+    """pl_snlm_2d_row_col runs the row pass into a transposed intermediate
+    (walk3 io=2: row staging + column flush on both passes); it must equal the
+    plain row pass -> column pass pair bit for bit, and the strided entry point
+    must reproduce both passes."""
+    b, r, c = shape
+    x = dev(np.random.default_rng(r + c).uniform(0, 255, shape).astype(np.float32))
+    row = pl.nlm_row_pass(x, p)
+    want = host(pl.nlm_col_pass(row, p))
+    assert np.array_equal(host(pl.snlm_2d_row_col(x, p)), want)
+    mid = torch.empty_like(x)
+    pl.nlm_pass_strided(x, mid, b, r, c, c, 1, 1, r, r * c, p)
+    assert np.array_equal(host(mid).reshape(b, c, r).transpose(0, 2, 1), host(row))
+    out = torch.empty_like(x)
+    pl.nlm_pass_strided(mid, out, b, c, r, r, 1, 1, c, r * c, p)
+    assert np.array_equal(host(out), want)
+    # plain layouts through the strided entry = the row / column pass APIs
+    pl.nlm_pass_strided(x, out, b, r, c, c, 1, c, 1, r * c, p)
+    assert np.array_equal(host(out), host(row))
+
+
 def test_guard_bands_no_stray_access():
     """Stand-in for compute-sanitizer (closed on this pool): every kernel path runs on
     inputs/outputs embedded in NaN guard bands.  A stray read poisons an output with
