@@ -114,13 +114,7 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
       const int ubase = c * R + BASE;
       const int pfirst = pos0 + ubase;
       const bool inside = MODE == 1 || (MODE == 0 && pfirst >= 0 && pfirst + R - 1 <= n - 1);
-#ifndef PLGPU_ABL_ROWSTAGE
-#define PLGPU_ABL_ROWSTAGE 0
-#endif
-      if constexpr (ROWS && PLGPU_ABL_ROWSTAGE) {
-        // ablation: stage only the first position row (timing experiment, wrong output)
-        if (lane < 16 && ubase >= 0) cp_async4(dstc + 2 * lane, rows_base + pfirst);
-      } else if constexpr (ROWS) {
+      if constexpr (ROWS) {
 #pragma unroll
         for (int qb = 0; qb < R; qb += 16) {
           const int q = qb + lane16;
@@ -428,10 +422,7 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
         __syncwarp();
       }
     }
-#ifndef PLGPU_ABL_ROWFLUSH
-#define PLGPU_ABL_ROWFLUSH 0
-#endif
-    if constexpr (OROWS && !PLGPU_ABL_ROWFLUSH) {
+    if constexpr (OROWS) {
       // flush this iteration's outputs: positions p = i0 + sb + q, q < R
       __syncwarp();
 #pragma unroll
