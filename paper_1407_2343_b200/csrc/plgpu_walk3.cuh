@@ -34,10 +34,11 @@ namespace plgpu {
 
 constexpr int kNS3 = 4;
 
-// Per warp: NS staging chunks + one output chunk, R rows each.
+// Per warp: NS staging chunks + one output chunk, R rows each; rounded up to
+// 16 bytes so every warp's ring (and its 16-byte flush rows) stays aligned.
 template <int ST, int LINES, bool ROWS>
 __host__ __device__ constexpr int pass3_smem_floats_per_warp() {
-  return (kNS3 + 1) * (ST + 1) * (32 * LINES + (ROWS ? 2 : 0));
+  return ((kNS3 + 1) * (ST + 1) * (32 * LINES + (ROWS ? 2 : 0)) + 3) / 4 * 4;
 }
 
 struct Pass3Desc {

@@ -351,6 +351,39 @@ def test_cpp_dropin_library():
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
 
 
+def test_hot_kernel_line_modes_bitwise(tmp_path):
+    """PLGPU_LINES / PLGPU_WPC pick the hot kernel's lines per lane and warps
+    per CTA (performance knobs only): every combination, with every staging /
+    flush mode (row pass, column pass, transposed-intermediate RC, S-NLM with
+    the fused average), gives the same bits."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import sys, numpy as np, torch; sys.path.insert(0, %r)\n"
+        "import paper_1407_2343_b200 as pl\n"
+        "rng = np.random.default_rng(8)\n"
+        "outs = {}\n"
+        "for (b, r, c, S, K) in [(2, 200, 256, 10, 3), (1, 130, 192, 15, 5), (1, 120, 96, 25, 7)]:\n"
+        "    x = torch.from_numpy(rng.uniform(0, 255, (b, r, c)).astype(np.float32)).cuda()\n"
+        "    p = (S, K, 40.0 + 5 * S)\n"
+        "    for nm, f in (('row', pl.nlm_row_pass), ('col', pl.nlm_col_pass),\n"
+        "                  ('rc', pl.snlm_2d_row_col), ('snlm', pl.snlm_2d)):\n"
+        "        outs[f'{S}_{nm}'] = f(x, p).cpu().numpy()\n"
+        "np.savez(sys.argv[1], **outs)\n" % os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    files = []
+    for env_extra in ({}, {"PLGPU_LINES": "1"}, {"PLGPU_LINES": "2"}, {"PLGPU_WPC": "8"},
+                      {"PLGPU_WPC": "2"}, {"PLGPU_LINES": "1", "PLGPU_WPC": "8"}):
+        f = str(tmp_path / f"o{len(files)}.npz")
+        r = subprocess.run([sys.executable, "-c", code, f], env=dict(os.environ, **env_extra),
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, (env_extra, r.stderr[-3000:])
+        files.append(np.load(f))
+    for other in files[1:]:
+        for key in files[0].files:
+            assert np.array_equal(files[0][key], other[key]), key
+
+
 def test_portable_and_production_walkers_bitwise_equal(tmp_path):
     """The production walker (smem-staged, packed f32x2) and the portable one
     (plgpu_walk.cuh) run the same per-line arithmetic: outputs are bitwise equal."""
