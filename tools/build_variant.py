@@ -16,13 +16,17 @@ def main():
     out = os.path.join("/tmp", f"plgpu_var_{tag}")
     os.makedirs(out, exist_ok=True)
     units = [(os.path.join(B.CSRC, "plgpu.cu"), os.path.join(out, "plgpu.o"))]
+    radii = [int(r) for r in os.environ["RADII"].split(",")] if os.environ.get("RADII") else B.WALK_RADII
     units += [(B._gen_inst(r), os.path.join(out, f"inst_S{r}.o")) for r in B.WALK_RADII]
+    # radii not rebuilt (RADII=10,15,25 for quick experiments) reuse the main build's objects
+    units = [(s, o if any(s.endswith(f"inst_S{r}.cu") for r in radii) or s.endswith("plgpu.cu")
+              else os.path.join(B.BUILD, "obj", os.path.basename(o))) for s, o in units]
 
     def one(so):
         B._run([B.NVCC] + B.NVFLAGS + extra + ["-c", so[0], "-o", so[1]])
 
     with ThreadPoolExecutor(os.cpu_count() or 4) as ex:
-        list(ex.map(one, units))
+        list(ex.map(one, [u for u in units if u[1].startswith(out)]))
     libdir = os.path.join(B.LIB, f"var_{tag}")
     os.makedirs(libdir, exist_ok=True)
     lib = os.path.join(libdir, "libplgpu.so")
