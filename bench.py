@@ -46,7 +46,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
-    ap.add_argument("--c5-dist", default="halo", choices=["halo", "slab"],
+    ap.add_argument("--c5-dist", default="halo", choices=["halo", "fused", "slab"],
                     help="c5 at N>1: row-partitioned halo exchange (default) or the "
                          "row-slab -> all-to-all -> column-slab transpose")
     return ap.parse_args()
@@ -74,8 +74,10 @@ def shard(n_items: int, world: int, rank: int):
 
 
 def dist_mode(cfg_name, world, how="halo"):
-    """c5 at N > 1 (one image): "halo" (row partition + halo exchange) or
-    "slab" (row slabs -> all-to-all -> column slabs); else None."""
+    """c5 at N > 1 (one image): "halo" (row partition + NCCL halo exchange),
+    "fused" (the same partition, halo rows stored into the neighbours'
+    symmetric-memory windows by the row-pass kernel itself) or "slab" (row
+    slabs -> all-to-all -> column slabs); else None."""
     return how if cfg_name == "c5" and world > 1 else None
 
 
@@ -283,7 +285,7 @@ def run_ours(args):
     params = (S, K, h)
     n_items = c.get("batch", 1)
     mode = dist_mode(args.config, world, args.c5_dist)
-    slab, halo = mode == "slab", mode == "halo"
+    slab, halo, fused = mode == "slab", mode in ("halo", "fused"), mode == "fused"
     if c["kind"] == "signal" or mode:
         lo, hi = 0, 1
     else:
@@ -313,7 +315,15 @@ def run_ours(args):
         win = torch.empty((whi - wlo, c["cols"]), dtype=x.dtype, device=dev)
         y = torch.empty((ohi - olo, c["cols"]), dtype=x.dtype, device=dev)
         p2p = []
-        for s_, d_, lo_, hi_ in plan.transfers():
+        if fused:
+            from paper_1407_2343_b200.distributed import symmetric_windows
+            windows, sym_barrier = symmetric_windows(plan, dev)
+            win = windows(rank)[:whi - wlo]
+            fan = [(windows(d_)[row_:row_ + (hi_ - lo_)], lo_ - olo, hi_ - olo)
+                   for d_, lo_, hi_, row_ in plan.fanout()]
+            if len(fan) > pl.PL_MAX_FANOUT:
+                raise RuntimeError("fused halo: more than PL_MAX_FANOUT neighbours")
+        for s_, d_, lo_, hi_ in ([] if fused else plan.transfers()):
             if s_ == rank:
                 p2p.append(torch.distributed.P2POp(torch.distributed.isend,
                                                    win[lo_ - wlo:hi_ - wlo], d_))
@@ -327,6 +337,9 @@ def run_ours(args):
         elif slab:
             pl.nlm_row_pass_blocked(x, params, cb, out=mid)
             torch.distributed.all_to_all_single(recv.reshape(-1), mid.reshape(-1))
+        elif fused:
+            pl.nlm_row_pass_fanout(x[0], params, out=win[olo - wlo:ohi - wlo], extras=fan)
+            sym_barrier()
         elif halo:
             pl.nlm_row_pass(x[0], params, out=win[olo - wlo:ohi - wlo])
             if p2p:
@@ -485,11 +498,13 @@ def run_ours(args):
                 line["config"]["nvlink_bytes_per_rank"] = plan.nvlink_bytes()
                 line["config"]["parallelism"] = f"row slabs -> all-to-all -> column slabs x{world}"
             else:
-                line["e2e"]["api"] = ("pinned H2D + row pass + NCCL halo send/recv + windowed "
-                                      "column pass + D2H")
+                line["e2e"]["api"] = ("pinned H2D + row pass + " +
+                                      ("fused NVLink halo stores (symmetric memory) + barrier"
+                                       if fused else "NCCL halo send/recv") +
+                                      " + windowed column pass + D2H")
                 line["config"]["nvlink_bytes_per_rank"] = plan.halo_bytes()
                 line["config"]["parallelism"] = (f"row partition (whole column segments) + "
-                                                 f"halo exchange x{world}")
+                                                 f"{'fused NVLink halo stores' if fused else 'halo exchange'} x{world}")
     elif not signal:
         hin = torch.from_numpy(imgs_host).pin_memory()
         hout = torch.empty_like(hin).pin_memory()

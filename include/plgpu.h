@@ -9,6 +9,7 @@
  *   pl_nlm_row_pass        nlm_row_pass                nlm.hpp:39-40, nlm.cpp:215-227
  *   pl_nlm_col_pass        nlm_col_pass                nlm.hpp:41-42, nlm.cpp:229-232
  *   pl_nlm_col_pass_window nlm_col_pass on a row window (multi-GPU halo form of the same)
+ *   pl_nlm_row_pass_fanout nlm_row_pass + fused halo stores into peers' windows (multi-GPU)
  *   pl_snlm_2d_row_col     snlm_2d_row_col             nlm.hpp:45-46, nlm.cpp:234-239
  *   pl_snlm_2d_col_row     snlm_2d_col_row             nlm.hpp:47-48, nlm.cpp:241-246
  *   pl_snlm_2d             snlm_2d (RC+CR)/2           nlm.hpp:51-52, nlm.cpp:248-253
@@ -145,6 +146,22 @@ int pl_nlm_pass_strided(const float* src, float* dst, int32_t batch, int32_t lin
  * multiple of col_block). */
 int pl_nlm_row_pass_blocked(const float* src, float* dst, int32_t batch, int32_t rows,
                             int32_t cols, int32_t col_block, pl_params p, void* stream);
+
+/* Row pass of ONE image whose output rows are also stored, as each tile is
+ * flushed, into up to PL_MAX_FANOUT extra destinations: rows [lo[x], hi[x])
+ * of the pass land at extra[x] + (r - lo[x]) * cols (row pitch cols).  With
+ * extra[x] a peer GPU's buffer mapped into this process (CUDA IPC / torch
+ * symmetric memory over NVLink), the halo exchange of the row-partitioned
+ * multi-GPU S-NLM is fused into the row pass: the neighbours' halo rows are
+ * written over NVLink by the same stores that write the local window, no
+ * separate collective.  dst is bit-identical to pl_nlm_row_pass and every
+ * extra row to the corresponding dst row.  Replaces the send/recv pair of the
+ * halo exchange (no reference counterpart: nlm_col_pass's transpose,
+ * core_types.cpp:90-98, is its single-node analogue). */
+#define PL_MAX_FANOUT 2
+int pl_nlm_row_pass_fanout(const float* src, float* dst, int32_t rows, int32_t cols, pl_params p,
+                           int32_t n_extra, float* const* extra, const int32_t* lo, const int32_t* hi,
+                           void* stream);
 
 /* Bytes of device workspace the composites need (0 for single passes). */
 size_t pl_workspace_bytes(int32_t op, int32_t batch, int32_t rows, int32_t cols);

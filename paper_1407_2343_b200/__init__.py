@@ -36,8 +36,9 @@ EXPORTS = [
     "pl_device_alloc", "pl_device_free", "pl_copy_to_device", "pl_copy_to_host",
     "pl_synchronize", "pl_distance_band_f32", "pl_distance_band_i32", "pl_banded_kernel_f64",
     "pl_col_window", "pl_nlm_col_pass_window", "pl_image_metrics_f32", "pl_image_metrics_f64",
-    "pl_nlm_pass_strided",
+    "pl_nlm_pass_strided", "pl_nlm_row_pass_fanout",
 ]
+PL_MAX_FANOUT = 2
 
 
 class ValidationError(ValueError):
@@ -95,6 +96,8 @@ def lib() -> C.CDLL:
             "pl_nlm_row_pass": ([vp, vp, i32, i32, i32, P, vp], C.c_int),
             "pl_nlm_col_pass": ([vp, vp, i32, i32, i32, P, vp], C.c_int),
             "pl_nlm_row_pass_blocked": ([vp, vp, i32, i32, i32, i32, P, vp], C.c_int),
+            "pl_nlm_row_pass_fanout": ([vp, vp, i32, i32, P, i32, C.POINTER(vp), C.POINTER(i32),
+                                        C.POINTER(i32), vp], C.c_int),
             "pl_col_window": ([i32, i32, i32, P] + [C.POINTER(i32)] * 4, C.c_int),
             "pl_image_metrics_f32": ([vp, vp, i32, i32, i32, vp, vp], C.c_int),
             "pl_nlm_pass_strided": ([vp, vp, i32, i32, i32, i64, i64, i64, i64, i64, P, vp],
@@ -263,6 +266,30 @@ def nlm_row_pass_blocked(x, p, col_block: int, out=None):
     out = torch.empty_like(x) if out is None else out
     _check(lib().pl_nlm_row_pass_blocked(x.data_ptr(), out.data_ptr(), b, r, c, int(col_block),
                                          _params(p), _stream(x)))
+    return out
+
+
+def nlm_row_pass_fanout(x, p, out=None, extras=()):
+    """Row pass of one image [rows, cols] that also stores output rows
+    [lo, hi) into each extra destination as it produces them.
+
+    ``extras``: up to PL_MAX_FANOUT (dst, lo, hi); dst is a device pointer
+    (int) or a tensor of >= (hi - lo) * cols floats, row pitch cols -- e.g. a
+    peer GPU's window buffer (torch symmetric memory): the fused halo
+    exchange of the row-partitioned multi-GPU path."""
+    import torch
+    _dev(x, torch.float32)
+    if x.dim() != 2:
+        raise ValueError("expected one image [rows, cols]")
+    r, c = x.shape
+    out = torch.empty_like(x) if out is None else out
+    n = len(extras)
+    ptrs = (C.c_void_p * max(1, n))(*[e[0] if isinstance(e[0], int) else e[0].data_ptr()
+                                      for e in extras])
+    lo = (C.c_int32 * max(1, n))(*[int(e[1]) for e in extras])
+    hi = (C.c_int32 * max(1, n))(*[int(e[2]) for e in extras])
+    _check(lib().pl_nlm_row_pass_fanout(x.data_ptr(), out.data_ptr(), r, c, _params(p), n, ptrs,
+                                        lo, hi, _stream(x)))
     return out
 
 

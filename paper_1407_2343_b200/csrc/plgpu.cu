@@ -198,6 +198,10 @@ int try_pass2(const plgpu::PassDesc& g, cudaStream_t st) {
   // segment portable walker wastes less.
   if (force_portable() || g.K > 7 || g.S < 1 || g.S > kMaxWalkS || g.lines_per_img < 16) return -1;
   const int ST = template_radius(g.S);
+  // fan-out stores: hot kernel's row flush or the portable walker
+  if (g.nx > 0 && (force_portable_v2() || plgpu::pass3_k_for(ST) != g.K || ST != g.S ||
+                   g.src_pos_stride != 1 || g.dst_pos_stride != 1))
+    return -1;
   const int LW = 32 * plgpu::pass2_lines(ST);
   const bool rows = g.src_pos_stride == 1 && g.dst_pos_stride == 1;
   const bool cols = g.src_line_stride == 1 && g.dst_line_stride == 1;
@@ -229,6 +233,12 @@ int try_pass2(const plgpu::PassDesc& g, cudaStream_t st) {
   d.K = g.K;
   d.coef = g.coef;
   d.scale = g.scale;
+  d.nx = g.nx;
+  for (int x = 0; x < 2; ++x) {
+    d.xdst[x] = g.xdst[x];
+    d.xlo[x] = g.xlo[x];
+    d.xhi[x] = g.xhi[x];
+  }
   d.avg = g.avg;
   const int64_t images = g.n_lines / g.lines_per_img;
   d.total_warps = images * d.groups_per_img * d.nseg;
@@ -641,6 +651,38 @@ int pl_nlm_pass_strided(const float* src, float* dst, int32_t batch, int32_t lin
   g.dst_pos_block = n;
   g.n = n;
   return run_pass(g, p, as_stream(stream));
+}
+
+int pl_nlm_row_pass_fanout(const float* src, float* dst, int32_t rows, int32_t cols, pl_params p,
+                           int32_t n_extra, float* const* extra, const int32_t* lo, const int32_t* hi,
+                           void* stream) {
+  int rc = validate_image(1, rows, cols);
+  if (!rc) rc = validate_params(p, cols);
+  if (!rc) rc = check_ptrs(src, dst);
+  if (rc) return rc;
+  if (n_extra < 0 || n_extra > PL_MAX_FANOUT || (n_extra > 0 && (!extra || !lo || !hi)))
+    return set_err(PL_ERR_ARG, "n_extra must be 0..PL_MAX_FANOUT with extra/lo/hi arrays");
+  for (int x = 0; x < n_extra; ++x)
+    if (!extra[x] || lo[x] < 0 || lo[x] > hi[x] || hi[x] > rows)
+      return set_err(PL_ERR_ARG, "fan-out rows must satisfy 0 <= lo <= hi <= rows, non-null extra");
+  cudaStream_t st = as_stream(stream);
+  plgpu::PassDesc g = row_desc(src, dst, 1, rows, cols);
+  const int S_eff = std::min<int>(p.search_radius, cols - 1);
+  if (S_eff < 1 || S_eff > kMaxWalkS) {  // direct route: pass, then copy the rows out
+    if ((rc = run_pass(g, p, st))) return rc;
+    for (int x = 0; x < n_extra; ++x)
+      if (hi[x] > lo[x])
+        PL_CUDA(cudaMemcpyAsync(extra[x], dst + (int64_t)lo[x] * cols,
+                                sizeof(float) * (size_t)(hi[x] - lo[x]) * cols, cudaMemcpyDefault, st));
+    return PL_OK;
+  }
+  g.nx = n_extra;
+  for (int x = 0; x < n_extra; ++x) {
+    g.xdst[x] = extra[x];
+    g.xlo[x] = lo[x];
+    g.xhi[x] = hi[x];
+  }
+  return run_pass(g, p, st);
 }
 
 int pl_nlm_row_pass_blocked(const float* src, float* dst, int32_t batch, int32_t rows,

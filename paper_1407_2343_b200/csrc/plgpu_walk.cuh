@@ -64,6 +64,12 @@ struct PassDesc {
   int32_t S;        // effective search radius, <= template S, <= n-1
   int32_t K;        // patch radius
   float coef;       // -log2(e) / h^2
+  // Fan-out (pl_nlm_row_pass_fanout, batch 1): output lines [xlo[x], xhi[x])
+  // are also stored at xdst[x] + (line - xlo[x]) * dst_line_stride + pos *
+  // dst_pos_stride as they are produced -- e.g. into a peer GPU's window.
+  float* xdst[2];
+  int32_t xlo[2], xhi[2];
+  int32_t nx;
 };
 
 __device__ __forceinline__ float ex2_approx(float x) {
@@ -104,7 +110,7 @@ __device__ __forceinline__ int mirror_pos(int p, int n) {
 template <int ST, bool EDGE>
 __device__ __forceinline__ void walk_segment(const PassDesc& g, const float* __restrict__ src,
                                              int64_t ps, float* __restrict__ dst, int64_t dps,
-                                             int s0, int s1) {
+                                             int s0, int s1, float* x0 = nullptr, float* x1 = nullptr) {
   constexpr int R = ST + 1;
   const int n = g.n;
   const int S = EDGE ? g.S : ST;
@@ -186,7 +192,10 @@ __device__ __forceinline__ void walk_segment(const PassDesc& g, const float* __r
         ad[rk] += w;
       }
       if (i >= s0) {
-        *op = epi(g.avg, g.dst, op, fminf(fmaxf(div_fix(num, den), lo), hi));
+        const float v = epi(g.avg, g.dst, op, fminf(fmaxf(div_fix(num, den), lo), hi));
+        *op = v;
+        if (x0) x0[(int64_t)i * dps] = v;  // fan-out (unblocked layout only)
+        if (x1) x1[(int64_t)i * dps] = v;
         op += dps;
         if (--orem == 0) {
           op += g.dst_block_stride - (int64_t)blk * dps;
@@ -217,11 +226,14 @@ __global__ void __launch_bounds__(128) nlm_pass_kernel(PassDesc g) {
   const int s0 = seg * g.seg_len;
   const int s1 = min(g.n, s0 + g.seg_len);
   const int i0 = max(0, s0 - g.S);
+  float* x[2] = {nullptr, nullptr};
+  for (int k = 0; k < g.nx; ++k)
+    if (li >= g.xlo[k] && li < g.xhi[k]) x[k] = g.xdst[k] + (li - g.xlo[k]) * g.dst_line_stride;
   const bool interior = (g.S == ST) && (i0 - 1 - g.K >= 0) && (s1 + g.K + g.S < g.n);
   if (interior)
-    walk_segment<ST, false>(g, src, g.src_pos_stride, dst, g.dst_pos_stride, s0, s1);
+    walk_segment<ST, false>(g, src, g.src_pos_stride, dst, g.dst_pos_stride, s0, s1, x[0], x[1]);
   else
-    walk_segment<ST, true>(g, src, g.src_pos_stride, dst, g.dst_pos_stride, s0, s1);
+    walk_segment<ST, true>(g, src, g.src_pos_stride, dst, g.dst_pos_stride, s0, s1, x[0], x[1]);
 }
 
 // ---------------------------------------------------------------------------

@@ -184,6 +184,12 @@ struct Pass2Desc {
   int32_t vec16;  // column pass: 16-byte copies legal (aligned, full line groups)
   int64_t total_warps;
   float coef;
+  // Fan-out (pl_nlm_row_pass_fanout, batch 1): output lines [xlo[x], xhi[x])
+  // are also stored at xdst[x] + (line - xlo[x]) * dst_line_stride + pos *
+  // dst_pos_stride as they are produced -- e.g. into a peer GPU's window.
+  float* xdst[2];
+  int32_t xlo[2], xhi[2];
+  int32_t nx;
 };
 
 constexpr int kCH = 16;  // positions per chunk

@@ -95,6 +95,9 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
   const int last_line = g.lines_per_img - 1;
   const int nchunks = (T + R - 1) / R;  // body iterations
   const bool full_group = l0 + LW - 1 <= last_line;
+  // fan-out lines in this group (warp-uniform; row flush only)
+  bool fan = false;
+  for (int x = 0; x < g.nx; ++x) fan |= l0 < g.xhi[x] && l0 + LW > g.xlo[x];
   // Column pass with 2 lines per lane: every lane stages (8-byte copies) and
   // flushes exactly the lines it computes -> no warp barriers around the ring.
   const bool own = !ROWS && LINES == 2 && g.vec16;
@@ -449,6 +452,16 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
             for (int j = 0; j < LW / 2; ++j) {
               const int l = 2 * j + half;
               if (l0 + l <= last_line) dbase[(int64_t)(l0 + l) * g.dst_line_stride] = orow[2 * j];
+            }
+          }
+          if (fan) {  // the same values into the fan-out destinations
+            for (int x = 0; x < g.nx; ++x) {
+#pragma unroll 4
+              for (int j = 0; j < LW / 2; ++j) {
+                const int line = l0 + 2 * j + half;
+                if (line <= last_line && line >= g.xlo[x] && line < g.xhi[x])
+                  g.xdst[x][(int64_t)(line - g.xlo[x]) * g.dst_line_stride + pofs] = orow[2 * j];
+              }
             }
           }
         }

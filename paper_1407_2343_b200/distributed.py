@@ -165,6 +165,18 @@ class HaloPlan:
                     out.append((s, d, lo, hi))
         return out
 
+    def fanout(self) -> list[tuple[int, int, int, int]]:
+        """Targets of the FUSED exchange (pl_nlm_row_pass_fanout): every
+        (dst_rank, lo, hi, dst_row) -- my row-pass output rows [lo, hi) are
+        stored straight into dst_rank's window, starting at its row dst_row."""
+        return [(d, lo, hi, lo - self.need[d][0]) for s, d, lo, hi in self.transfers()
+                if s == self.rank]
+
+    @property
+    def window_capacity(self) -> int:
+        """Rows of the largest window (symmetric buffers are equal-sized)."""
+        return max([hi - lo for lo, hi in self.need] + [1])
+
     def halo_bytes(self, itemsize: int = 4) -> int:
         """Bytes this rank receives over NVLink."""
         return sum((hi - lo) * self.W * itemsize for s, d, lo, hi in self.transfers()
@@ -207,6 +219,76 @@ def halo_rc(x_rows, params, plan: HaloPlan, *, row_pass: Callable | None = None,
         exchange(ops)
     a, b = plan.segments
     return col_pass_window(y, wlo, plan.H, a, b, params)
+
+
+def halo_rows_fused(x_rows, params, plan: HaloPlan, windows: Callable, *,
+                    row_pass_fanout: Callable | None = None):
+    """Phase 1 of the fused halo path: the row pass on my rows writes its output
+    into my window AND, in the same kernel, the rows my neighbours need into
+    their windows (peer memory over NVLink; pl_nlm_row_pass_fanout).
+
+    ``windows(rank)`` -> that rank's window buffer [>= window rows, W] as seen
+    from this process (torch symmetric memory ``get_buffer``, or plain device
+    tensors when G ranks are emulated on one GPU).  Targets beyond the kernel's
+    PL_MAX_FANOUT are copied after the pass."""
+    import paper_1407_2343_b200 as pl
+    if row_pass_fanout is None:
+        row_pass_fanout = pl.nlm_row_pass_fanout
+    olo, ohi = plan.rows
+    wlo, _ = plan.window_rows
+    if ohi <= olo:
+        return
+    y = windows(plan.rank)
+    targets = plan.fanout()
+    fused = [(windows(d)[row:row + (hi - lo)], lo - olo, hi - olo)
+             for d, lo, hi, row in targets[:pl.PL_MAX_FANOUT]]
+    mine = y[olo - wlo:ohi - wlo]
+    row_pass_fanout(x_rows, params, out=mine, extras=fused)
+    for d, lo, hi, row in targets[pl.PL_MAX_FANOUT:]:
+        windows(d)[row:row + (hi - lo)].copy_(mine[lo - olo:hi - olo])
+
+
+def halo_cols_fused(params, plan: HaloPlan, windows: Callable, *,
+                    col_pass_window: Callable | None = None):
+    """Phase 2: the windowed column pass on my (now complete) window."""
+    if col_pass_window is None:
+        import paper_1407_2343_b200 as pl
+        col_pass_window = pl.nlm_col_pass_window
+    wlo, whi = plan.window_rows
+    a, b = plan.segments
+    if plan.rows[1] <= plan.rows[0]:
+        return None
+    return col_pass_window(windows(plan.rank)[:whi - wlo], wlo, plan.H, a, b, params)
+
+
+def halo_rc_fused(x_rows, params, plan: HaloPlan, windows: Callable, barrier: Callable, *,
+                  row_pass_fanout: Callable | None = None, col_pass_window: Callable | None = None):
+    """Row pass with fused halo stores -> barrier -> windowed column pass.
+    ``barrier()`` must order every rank's row pass (and its peer stores)
+    before any column pass, e.g. the symmetric-memory handle's device
+    barrier on the current stream."""
+    halo_rows_fused(x_rows, params, plan, windows, row_pass_fanout=row_pass_fanout)
+    barrier()
+    return halo_cols_fused(params, plan, windows, col_pass_window=col_pass_window)
+
+
+def symmetric_windows(plan: HaloPlan, device, group=None):
+    """Equal-sized window buffers in torch symmetric memory (one per rank,
+    peer-mapped over NVLink).  Returns (windows, barrier) for halo_rc_fused."""
+    import torch
+    import torch.distributed as dist
+    import torch.distributed._symmetric_memory as symm
+    shape = (plan.window_capacity, plan.W)
+    buf = symm.empty(*shape, dtype=torch.float32, device=device)
+    hdl = symm.rendezvous(buf, group or dist.group.WORLD)
+    views = {plan.rank: buf}
+
+    def windows(r):
+        if r not in views:
+            views[r] = hdl.get_buffer(r, shape, torch.float32)
+        return views[r]
+
+    return windows, (lambda: hdl.barrier(channel=0))
 
 
 def _p2p_exchange(ops):

@@ -13,8 +13,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_1407_2343_b200.distributed import (HaloPlan, SlabPlan, blocked_layout, halo_rc, shard,
-                                              slab_rc)
+from paper_1407_2343_b200.distributed import (HaloPlan, SlabPlan, blocked_layout, halo_rc,
+                                              halo_rc_fused, shard, slab_rc)
 
 
 def test_shard_covers_batch():
@@ -184,3 +184,102 @@ def test_halo_exchange_matches_single_process(world):
     assert all(ok for _, ok, _ in results), results
     if world >= 4:
         assert max(n for _, _, n in results) >= 2  # some window spans several owners
+
+
+@pytest.mark.parametrize("H,W,world,p", [(16384, 16384, 2, (25, 7, 25.0)), (16384, 16384, 4, (25, 7, 25.0)),
+                                         (16384, 16384, 8, (25, 7, 25.0)), (160, 24, 4, (4, 1, 30.0)),
+                                         (4096, 64, 3, (15, 5, 50.0))])
+def test_halo_fanout_plan(H, W, world, p):
+    """The fused exchange's targets (HaloPlan.fanout) are exactly the plan's
+    transfers, land inside the destination's window, and together with the
+    destination's own rows cover its whole window; c5 needs <= 2 (the kernel's
+    PL_MAX_FANOUT) targets per rank."""
+    import paper_1407_2343_b200 as pl
+    plans = [HaloPlan(H, W, world, r, p) for r in range(world)]
+    for r, plan in enumerate(plans):
+        fan = plan.fanout()
+        assert [(r, d, lo, hi) for d, lo, hi, _ in fan] == [t for t in plan.transfers() if t[0] == r]
+        for d, lo, hi, row in fan:
+            wlo, whi = plans[d].window_rows
+            assert row == lo - wlo and 0 <= row and row + (hi - lo) <= whi - wlo
+            assert whi - wlo <= plan.window_capacity
+        if H == 16384:
+            assert len(fan) <= pl.PL_MAX_FANOUT
+    for d, plan in enumerate(plans):
+        wlo, whi = plan.window_rows
+        have = np.zeros(whi - wlo, bool)
+        olo, ohi = plan.rows
+        have[olo - wlo:ohi - wlo] = True
+        for s_, other in enumerate(plans):
+            for dd, lo, hi, row in other.fanout():
+                if dd == d:
+                    have[row:row + hi - lo] = True
+        assert have.all() or ohi <= olo
+
+
+def _fused_worker(rank, world, port, H, W, params, wins, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    os.environ["PLGPU_SEG"] = "16"
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import Oracle
+        from paper_1407_2343_b200 import col_window, workloads
+
+        orc = Oracle.get()
+        S, K, h = params
+        img = workloads.make_image(H, W, 12, 20.0, seed=12).astype(np.float64)
+        plan = HaloPlan(H, W, world, rank, params)
+
+        def row_pass_fanout(x, p, out, extras):
+            # CPU stand-in for pl_nlm_row_pass_fanout: every produced row goes
+            # to my window and straight into the peers' (shared-memory) windows
+            y = torch.from_numpy(orc.row_pass(x.numpy(), S, K, h))
+            out.copy_(y)
+            for dst, lo, hi in extras:
+                dst.copy_(y[lo:hi])
+
+        def naive_cols(full):
+            return np.stack([orc.nlm_1d(full[:, c], S, K, h, naive=True)
+                             for c in range(full.shape[1])], axis=1)
+
+        def col_pass_window(y, in_lo, H_, a, b, p):
+            full = np.full((H_, W), np.nan)  # reads outside the window poison the result
+            full[in_lo:in_lo + y.shape[0]] = y.numpy()
+            _, _, out_lo, out_hi = col_window(H_, a, b, p)
+            return torch.from_numpy(naive_cols(full)[out_lo:out_hi])
+
+        r0, r1 = plan.rows
+        got = halo_rc_fused(torch.from_numpy(img[r0:r1].copy()), params, plan, lambda r: wins[r],
+                            dist.barrier, row_pass_fanout=row_pass_fanout,
+                            col_pass_window=col_pass_window)
+        want = naive_cols(orc.row_pass(img, S, K, h))[r0:r1]
+        ok = got.shape == want.shape and bool(np.array_equal(got.numpy(), want))
+        out_q.put((rank, ok, len(plan.fanout())))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_fused_halo_matches_single_process(world):
+    """The fused halo path's host logic (fan-out targets, peer windows, barrier,
+    windowed column pass) across gloo processes; peer windows are shared-memory
+    tensors standing in for NVLink-mapped symmetric memory."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    H, W = 160, 24
+    params = (4, 1, 30.0)
+    wins = [torch.full((H, W), float("nan"), dtype=torch.float64).share_memory_()
+            for _ in range(world)]
+    port = _free_port()
+    procs = [ctx.Process(target=_fused_worker, args=(r, world, port, H, W, params, wins, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert all(ok for _, ok, _ in results), results
+    if world >= 4:
+        assert max(n for _, _, n in results) > 2  # the post-pass copy route is exercised too

@@ -499,6 +499,86 @@ def test_halo_exchange_emulated_bitwise(G, S, K):
     assert np.array_equal(got, want)
 
 
+@pytest.mark.parametrize("rows,cols,S,K", [(300, 517, 10, 3), (200, 300, 25, 7), (160, 256, 15, 5),
+                                           (130, 200, 5, 2), (64, 90, 0, 2), (40, 300, 10, 9)])
+def test_row_pass_fanout_bitwise(rows, cols, S, K):
+    """pl_nlm_row_pass_fanout: dst is bit-identical to the plain row pass and
+    every fanned-out row to the corresponding dst row (hot kernel's row flush,
+    portable walker, direct route + copies); nothing outside the targets is
+    written."""
+    img = np.random.default_rng(rows + S).uniform(0, 255, (rows, cols)).astype(np.float32)
+    p = (S, K, 60.0)
+    x = dev(img)
+    want = host(pl.nlm_row_pass(x, p))
+    ranges = [(0, min(rows, 37)), (max(0, rows - 50), rows)]
+    bufs = [torch.full((hi - lo + 3, cols), float("nan"), device="cuda") for lo, hi in ranges]
+    out = pl.nlm_row_pass_fanout(x, p, extras=[(b, lo, hi) for b, (lo, hi) in zip(bufs, ranges)])
+    assert np.array_equal(host(out), want)
+    for b, (lo, hi) in zip(bufs, ranges):
+        got = host(b)
+        assert np.array_equal(got[:hi - lo], want[lo:hi])
+        assert np.isnan(got[hi - lo:]).all()
+    assert np.array_equal(host(pl.nlm_row_pass_fanout(x, p)), want)  # no targets
+    with pytest.raises(RuntimeError):  # PL_ERR_ARG: more than PL_MAX_FANOUT targets
+        pl.nlm_row_pass_fanout(x, p, extras=[(bufs[0], 0, 1)] * 3)
+    with pytest.raises(RuntimeError):  # PL_ERR_ARG: rows outside the image
+        pl.nlm_row_pass_fanout(x, p, extras=[(bufs[0], 5, rows + 1)])
+
+
+@pytest.mark.parametrize("G,S,K", [(4, 10, 3), (8, 25, 7), (3, 15, 5), (2, 25, 7)])
+def test_fused_halo_emulated_bitwise(G, S, K):
+    """The fused halo path with G ranks emulated on one GPU: each rank's row
+    pass (pl_nlm_row_pass_fanout) stores its halo rows straight into the other
+    ranks' window buffers (NaN-filled: any row not delivered shows), then the
+    windowed column passes; the stitched rows equal the single-device RC bit
+    for bit.  No rank waits on another inside a kernel: phase 1 runs for every
+    rank, then phase 2."""
+    from paper_1407_2343_b200.distributed import HaloPlan, halo_cols_fused, halo_rows_fused
+    H, W = 8192, 96
+    p = (S, K, 60.0)
+    img = workloads.make_image(H, W, 40, 25.0, seed=9)
+    want = host(pl.snlm_2d_row_col(dev(img), p))
+    plans = [HaloPlan(H, W, G, r, p) for r in range(G)]
+    cap = plans[0].window_capacity
+    wins = [torch.full((cap, W), float("nan"), device="cuda") for _ in range(G)]
+    for r, plan in enumerate(plans):
+        olo, ohi = plan.rows
+        halo_rows_fused(dev(img[olo:ohi]), p, plan, lambda q: wins[q])
+    got = np.concatenate([host(halo_cols_fused(p, plans[r], lambda q: wins[q])) for r in range(G)])
+    assert np.array_equal(got, want)
+
+
+def test_symmetric_windows_fused_rc(tmp_path):
+    """The fused halo path end to end through torch symmetric memory
+    (rendezvous, peer-buffer views, device barrier) under torchrun with one
+    rank -- the setup bench.py --c5-dist fused runs at N > 1."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "symm.py"
+    script.write_text(
+        "import sys, torch, torch.distributed as dist\n"
+        f"sys.path.insert(0, {root!r})\n"
+        "torch.cuda.set_device(0)\n"
+        "dist.init_process_group('nccl', device_id=torch.device('cuda', 0))\n"
+        "import paper_1407_2343_b200 as pl\n"
+        "from paper_1407_2343_b200 import workloads\n"
+        "from paper_1407_2343_b200.distributed import HaloPlan, symmetric_windows, halo_rc_fused\n"
+        "p = (25, 7, 136.9)\n"
+        "plan = HaloPlan(4096, 256, 1, 0, p)\n"
+        "windows, barrier = symmetric_windows(plan, torch.device('cuda', 0))\n"
+        "img = torch.from_numpy(workloads.make_image(4096, 256, 20, 25.0, seed=3)).cuda()\n"
+        "got = halo_rc_fused(img, p, plan, windows, barrier)\n"
+        "assert torch.equal(got, pl.snlm_2d_row_col(img, p))\n"
+        "print('SYMM_OK')\n"
+        "dist.destroy_process_group()\n")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
+                        "--master-addr", "127.0.0.1", "--master-port", "29561", str(script)],
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "SYMM_OK" in r.stdout, (r.stdout[-2000:], r.stderr[-3000:])
+
+
 @pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
 def test_image_metrics_vs_oracle(dtype):
     """Device MSE / PSNR / SSIM (metrics.cpp:98-158) against the oracle on the
