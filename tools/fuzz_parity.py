@@ -1,0 +1,94 @@
+"""Randomised parity sweep on the GPU (test infrastructure: uses oracle/).
+
+Each case draws a shape (batch, rows, cols), (S, K, h), data kind (uniform,
+integer-valued, the configs' synthetic image, near-constant) and checks, for
+every single pass the CUDA result against the oracle at T2 * max(1, (25/h)^2)
+and every two-pass composite at T2 * max(1, (32/h)^2) (T2 = 1e-3 on the
+[0, 255] scale, scaled with the data range; the small-h terms are the fp32
+running sums' and the second pass's conditioning), and the
+bitwise invariants
+(transpose equivariance, batch invariance, snlm = (RC + CR) / 2).  Hot (K, S)
+pairs are drawn often so the specialised kernel's edge / masked / partial-
+group paths get covered.
+
+    python tools/fuzz_parity.py --seconds 300 [--seed 1]
+"""
+import argparse
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    import torch
+    import paper_1407_2343_b200 as pl
+    from paper_1407_2343_b200 import workloads
+    from oracle import Oracle
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--seconds", type=float, default=120)
+    ap.add_argument("--seed", type=int, default=1)
+    a = ap.parse_args()
+    rng = np.random.default_rng(a.seed)
+    orc = Oracle.get()
+    hot = [(10, 3), (15, 5), (25, 7)]
+    t0, n, worst, fails = time.time(), 0, 0.0, []
+    while time.time() - t0 < a.seconds:
+        if rng.uniform() < 0.6:
+            S, K = hot[rng.integers(0, 3)]
+        else:
+            S, K = int(rng.integers(0, 33)), int(rng.integers(0, 9))
+        b = int(rng.integers(1, 4))
+        r, c = int(rng.integers(1, 420)), int(rng.integers(1, 420))
+        if K > min(r, c):
+            continue
+        kind = rng.integers(0, 4)
+        if kind == 0:
+            x = rng.uniform(0, 255, (b, r, c))
+        elif kind == 1:
+            x = rng.integers(0, 256, (b, r, c)).astype(np.float64)
+        elif kind == 2:
+            x = np.stack([workloads.make_image(r, c, 8, 20.0, seed=int(rng.integers(1 << 30)))
+                          for _ in range(b)]).astype(np.float64)
+        else:
+            x = 100.0 + rng.uniform(0, 1e-3, (b, r, c))
+        h = float(np.exp(rng.uniform(np.log(5.0), np.log(2000.0))))
+        p = (S, K, h)
+        x32 = x.astype(np.float32)
+        xd = torch.from_numpy(x32).cuda()
+        scale = max(1.0, float(np.abs(x32).max()) / 255.0)
+        try:
+            out = {}
+            for op, fn in (("rc", pl.snlm_2d_row_col), ("cr", pl.snlm_2d_col_row),
+                           ("snlm", pl.snlm_2d), ("row", pl.nlm_row_pass), ("col", pl.nlm_col_pass)):
+                out[op] = fn(xd, p).cpu().numpy()
+            for op, v in out.items():
+                h0 = 25.0 if op in ("row", "col") else 32.0
+                tol = 1e-3 * scale * max(1.0, (h0 / h) ** 2)
+                for i in range(b):
+                    want = orc.filter(op, x32[i].astype(np.float64), S, K, h, threads=8)
+                    err = float(np.abs(v[i].astype(np.float64) - want).max())
+                    worst = max(worst, err / tol)
+                    assert err <= tol, (op, i, err)
+            xt = torch.from_numpy(np.ascontiguousarray(x32.transpose(0, 2, 1))).cuda()
+            assert np.array_equal(pl.snlm_2d_col_row(xt, p).cpu().numpy(),
+                                  out["rc"].transpose(0, 2, 1)), "transpose equivariance"
+            assert np.array_equal(out["snlm"], (out["rc"] + out["cr"]) / np.float32(2)), "snlm mean"
+            one = pl.snlm_2d_row_col(xd[b - 1:b].contiguous(), p).cpu().numpy()
+            assert np.array_equal(one[0], out["rc"][b - 1]), "batch invariance"
+        except AssertionError as e:
+            fails.append(((b, r, c), p, int(kind), str(e)))
+            print("FAIL", fails[-1], flush=True)
+        n += 1
+    print(f"fuzz: {n} cases in {time.time() - t0:.0f} s, {len(fails)} failures, "
+          f"worst error / tolerance {worst:.3g}")
+    sys.exit(1 if fails else 0)
+
+
+if __name__ == "__main__":
+    main()
