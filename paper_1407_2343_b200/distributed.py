@@ -281,12 +281,14 @@ def symmetric_windows(plan: HaloPlan, device, group=None):
     shape = (plan.window_capacity, plan.W)
     buf = symm.empty(*shape, dtype=torch.float32, device=device)
     hdl = symm.rendezvous(buf, group or dist.group.WORLD)
-    views = {plan.rank: buf}
+    views = {}
 
-    def windows(r):
+    def windows(r):  # every rank's buffer through the handle (own one included)
         if r not in views:
             views[r] = hdl.get_buffer(r, shape, torch.float32)
         return views[r]
+
+    windows.keepalive = buf
 
     return windows, (lambda: hdl.barrier(channel=0))
 
