@@ -71,7 +71,7 @@ void launch_pass2(const Pass2Desc& g, bool rows, cudaStream_t st) {
 
 template <int ST, int KT, int L, int IO, int WPC, bool AVG>
 void launch3(const Pass3Desc& d, cudaStream_t st) {
-  const size_t smem = sizeof(float) * WPC * pass3_smem_floats_per_warp<ST, L, IO != 0>();
+  const size_t smem = sizeof(float) * WPC * pass3_smem_floats_per_warp<ST, L, IO>();
   unsigned grid;
   if constexpr (WPC == 8) {  // 8 line groups of one segment per CTA
     const int64_t groups = d.b.total_warps / d.b.nseg;

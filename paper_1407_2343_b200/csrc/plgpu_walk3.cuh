@@ -16,7 +16,10 @@
 //    PITCH = LW + 2 floats; 16 lanes write 16 consecutive positions of one line
 //    -> banks (2u + l) mod 32 are distinct, and the compute reads (LDS.64 of
 //    lines 2l, 2l+1) are contiguous.  Outputs are staged the same way and
-//    leave once per iteration as contiguous row pieces.
+//    leave once per iteration as contiguous row pieces.  The 2-line
+//    transposed-intermediate passes (io 2) copy 4 positions x 8 lines per
+//    instruction instead (immediate position offsets, one address add per
+//    8 lines; pitch LW + 8).
 //  * One instantiation per configuration: chunks inside the line take the fast
 //    copy path, chunks touching a line end the mirrored one (per chunk, at run
 //    time); every iteration that needs no window clipping runs the branch-free
@@ -36,9 +39,22 @@ constexpr int kNS3 = 4;
 
 // Per warp: NS staging chunks + one output chunk, R rows each; rounded up to
 // 16 bytes so every warp's ring (and its 16-byte flush rows) stays aligned.
-template <int ST, int LINES, bool ROWS>
+// 2-line io-2 staging copies 4 positions x 8 lines per instruction (c4:
+// +2 %); with 1 line per lane it measured slower (c3 -2 %, c5 -11 %).
+template <int LINES, int IO>
+__host__ __device__ constexpr bool pass3_copy8x4() {
+  return IO == 2 && LINES == 2;
+}
+// Row pitch of the staging ring: io 0 rows of LW lines; the transposing
+// copies of 16 positions x 2 lines (io 1, 1-line io 2) and the row flush are
+// conflict-free at LW + 2, the 4-positions x 8-lines copies at LW + 8.
+template <int LINES, int IO>
+__host__ __device__ constexpr int pass3_pitch() {
+  return 32 * LINES + (pass3_copy8x4<LINES, IO>() ? 8 : IO != 0 ? 2 : 0);
+}
+template <int ST, int LINES, int IO>
 __host__ __device__ constexpr int pass3_smem_floats_per_warp() {
-  return ((kNS3 + 1) * (ST + 1) * (32 * LINES + (ROWS ? 2 : 0)) + 3) / 4 * 4;
+  return ((kNS3 + 1) * (ST + 1) * pass3_pitch<LINES, IO>() + 3) / 4 * 4;
 }
 
 struct Pass3Desc {
@@ -72,7 +88,7 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
   constexpr int LW = 32 * LINES;
   constexpr int R = ST + 1;
   constexpr int BASE = ST + 2 * KT + 2;
-  constexpr int PITCH = LW + (ROWS ? 2 : 0);
+  constexpr int PITCH = pass3_pitch<LINES, IO>();
   constexpr int CHUNK = R * PITCH;  // floats per chunk slot
   constexpr int M = (BASE + R - 1) / R;  // chunks before chunk 0 (init window)
   static_assert(2 * KT + 2 <= R, "iteration must read at most two chunks");
@@ -125,19 +141,38 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
           if (q < R && ubase + q >= 0) {
             const int p = pfirst + q;
             float* drow = dstc + q * PITCH + half;
-            if (inside && full_group) {
+            if (inside && full_group && !pass3_copy8x4<LINES, IO>()) {
               const float* gp = rows_base + p;
 #pragma unroll 8
               for (int j = 0; j < LW / 2; ++j) {
                 cp_async4(drow + 2 * j, gp);
                 gp += 2 * ls;
               }
-            } else {
+            } else if (!(inside && full_group)) {
               const float* col = src + (int64_t)mirror_pos(p, n) * ps;
 #pragma unroll 4
               for (int j = 0; j < LW / 2; ++j)
                 cp_async4(drow + 2 * j, col + (int64_t)min(l0 + 2 * j + half, last_line) * ls);
             }
+          }
+        }
+        if (pass3_copy8x4<LINES, IO>() && inside && full_group) {
+          // 4 positions x 8 lines per copy instruction (pp = lane & 3,
+          // lg = lane >> 2): the positions step by immediate offsets, the
+          // lines by one 64-bit add per 8-line group; 8-16 L1 sectors per copy
+          const int pp = lane & 3, lg = lane >> 2;
+          const float* gl = src + (int64_t)(l0 + lg) * ls + pfirst + pp;
+          float* dl = dstc + pp * PITCH + lg;
+          const int64_t gstep = 8 * ls;
+#pragma unroll
+          for (int g8 = 0; g8 < LW / 8; ++g8) {
+#pragma unroll
+            for (int t = 0; t < (R + 3) / 4; ++t) {
+              const int q = 4 * t + pp;
+              if (q < R && ubase + q >= 0) cp_async4(dl + 4 * t * PITCH, gl + 4 * t);
+            }
+            gl += gstep;
+            dl += 8;
           }
         }
       } else if (own) {
@@ -482,7 +517,7 @@ __global__ void __launch_bounds__(32 * WPC, 1)
   const Pass2Desc& g = d.b;
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
-  float* ring = smem + wib * pass3_smem_floats_per_warp<ST, LINES, IO != 0>();
+  float* ring = smem + wib * pass3_smem_floats_per_warp<ST, LINES, IO>();
   if constexpr (WPC == 8) {
     const int bpi = (g.groups_per_img + 7) / 8;  // 8-group blocks per image
     const int64_t blocks_per_seg = (g.total_warps / g.nseg + 0) / g.groups_per_img * bpi;
