@@ -398,20 +398,28 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
         const float* sp = oring + LINES * lane;
         if constexpr (AVG) {  // fused S-NLM average: all partner loads before any store
           const float2* ap = reinterpret_cast<const float2*>(g.avg + (dp - g.dst));
+          const bool whole = i0 + sb >= s0 && i0 + sb + R <= s1;
           float2 a[R];
 #pragma unroll
           for (int q = 0; q < R; ++q) {
             const int p = i0 + sb + q;
-            a[q] = (p >= s0 && p < s1) ? __ldg(ap) : make_float2(0.f, 0.f);
+            a[q] = (whole || (p >= s0 && p < s1)) ? __ldg(ap) : make_float2(0.f, 0.f);
             ap += g.dst_pos_stride / 2;
           }
 #pragma unroll
           for (int q = 0; q < R; ++q) {
             const int p = i0 + sb + q;
-            if (p >= s0 && p < s1) {
+            if (whole || (p >= s0 && p < s1)) {
               const float2 v = *reinterpret_cast<const float2*>(sp);
               *reinterpret_cast<float2*>(dp) = make_float2((a[q].x + v.x) / 2.0f, (a[q].y + v.y) / 2.0f);
             }
+            dp += g.dst_pos_stride;
+            sp += OPITCH;
+          }
+        } else if (i0 + sb >= s0 && i0 + sb + R <= s1) {  // whole iteration inside [s0, s1)
+#pragma unroll
+          for (int q = 0; q < R; ++q) {
+            *reinterpret_cast<float2*>(dp) = *reinterpret_cast<const float2*>(sp);
             dp += g.dst_pos_stride;
             sp += OPITCH;
           }
@@ -428,20 +436,26 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
         __syncwarp();
         constexpr int LPR = LW / 4;  // lanes per row, 16 B each
 #pragma unroll
-        for (int qb = 0; qb < R; qb += 32 / LPR) {
-          const int q = qb + lane / LPR;
-          const int p = i0 + sb + q;
-          if (q < R && p >= s0 && p < s1) {
-            float4 v = *reinterpret_cast<const float4*>(oring + q * OPITCH + 4 * (lane % LPR));
-            const int64_t off = dst_img + (int64_t)p * g.dst_pos_stride + l0 + 4 * (lane % LPR);
-            if constexpr (AVG) {  // fused S-NLM average
-              const float4 a = __ldg(reinterpret_cast<const float4*>(g.avg + off));
-              v = make_float4((a.x + v.x) / 2.0f, (a.y + v.y) / 2.0f, (a.z + v.z) / 2.0f,
-                              (a.w + v.w) / 2.0f);
+        auto flush16 = [&](auto check_tag) {
+          constexpr bool CHECK = decltype(check_tag)::value;
+#pragma unroll
+          for (int qb = 0; qb < R; qb += 32 / LPR) {
+            const int q = qb + lane / LPR;
+            const int p = i0 + sb + q;
+            if (q < R && (!CHECK || (p >= s0 && p < s1))) {
+              float4 v = *reinterpret_cast<const float4*>(oring + q * OPITCH + 4 * (lane % LPR));
+              const int64_t off = dst_img + (int64_t)p * g.dst_pos_stride + l0 + 4 * (lane % LPR);
+              if constexpr (AVG) {  // fused S-NLM average
+                const float4 a = __ldg(reinterpret_cast<const float4*>(g.avg + off));
+                v = make_float4((a.x + v.x) / 2.0f, (a.y + v.y) / 2.0f, (a.z + v.z) / 2.0f,
+                                (a.w + v.w) / 2.0f);
+              }
+              *reinterpret_cast<float4*>(g.dst + off) = v;
             }
-            *reinterpret_cast<float4*>(g.dst + off) = v;
           }
-        }
+        };
+        if (i0 + sb >= s0 && i0 + sb + R <= s1) flush16(std::integral_constant<bool, false>{});
+        else flush16(std::integral_constant<bool, true>{});
         __syncwarp();
       } else {
         __syncwarp();
