@@ -281,7 +281,10 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
   const int64_t dst_img = img * g.dst_img_stride;
   const int my_line = l0 + lane * LINES;
 
-  for (int c = 0; c < nchunks; ++c) {
+  // One chunk iteration (staging, R-step body, flush).  Clean iterations
+  // (no masking) form a prefix of the loop and run in a loop of their own, so
+  // the hot loop has a single body and no merge at its back edge.
+  auto iteration = [&](const int c, auto mask_tag) {
     // Lockstep CTAs (large S): every warp of the CTA starts each iteration
     // together, so the SM's warps stream the (large) unrolled body through the
     // instruction cache once instead of once per warp.
@@ -381,15 +384,7 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
         nr[r] = sc(at(r, BASE));
       }
     };
-    if constexpr (MODE == 1) {
-      body(std::integral_constant<bool, false>{});
-    } else if constexpr (MODE == 2) {
-      body(std::integral_constant<bool, true>{});
-    } else {
-      const bool clean = S == ST && sb + R <= T && i0 + sb + R - 1 + ST <= n - 1;
-      if (clean) body(std::integral_constant<bool, false>{});
-      else body(std::integral_constant<bool, true>{});
-    }
+    body(mask_tag);
 
     if constexpr (!OROWS) {
       // flush this iteration's outputs (row q = position i0 + sb + q)
@@ -517,6 +512,19 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
       }
       __syncwarp();
     }
+  };
+  using Clean = std::integral_constant<bool, false>;
+  using Masked = std::integral_constant<bool, true>;
+  if constexpr (MODE == 1) {
+    for (int c = 0; c < nchunks; ++c) iteration(c, Clean{});
+  } else if constexpr (MODE == 2) {
+    for (int c = 0; c < nchunks; ++c) iteration(c, Masked{});
+  } else {
+    // iteration c is clean iff S == ST, (c+1)R <= T and i0 + (c+1)R - 1 + ST <= n - 1
+    const int nclean = S == ST ? min(T / R, max(0, (n - ST - i0) / R)) : 0;
+    int c = 0;
+    for (; c < nclean; ++c) iteration(c, Clean{});
+    for (; c < nchunks; ++c) iteration(c, Masked{});
   }
   cp_wait<0>();
 }
