@@ -42,6 +42,13 @@ __device__ __forceinline__ F2 f2_make(float a, float b) {
 __device__ __forceinline__ void f2_split(F2 v, float& a, float& b) {
   asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v.r));
 }
+// {a, v.hi}: the high half flows from v, so a ring slot whose high half is a
+// constant keeps it in place instead of re-materialising it on every refill.
+__device__ __forceinline__ F2 f2_set_lo(F2 v, float a) {
+  F2 o;
+  asm("{.reg .f32 l, h; mov.b64 {l, h}, %1; mov.b64 %0, {%2, h};}" : "=l"(o.r) : "l"(v.r), "f"(a));
+  return o;
+}
 
 template <int LINES>
 struct VecOps;
