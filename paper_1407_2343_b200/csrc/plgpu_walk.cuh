@@ -142,8 +142,8 @@ __device__ __forceinline__ void walk_segment(const PassDesc& g, const float* __r
     hi = fmaxf(hi, fr[q]);
     nr[q] = lds(i0 + K + q);
     orr[q] = lds(i0 - 1 - K + q);
-    an[q] = 0.f;
-    ad[q] = 0.f;
+    an[q] = fr[q];  // the centre sample (w = 1) starts each pixel's sums
+    ad[q] = 1.f;
     d[q] = 0.f;
   }
   // Anchor: d_k(i0-1) by a direct (2K+1)-term sum, t ascending.
@@ -174,8 +174,8 @@ __device__ __forceinline__ void walk_segment(const PassDesc& g, const float* __r
       const float to = lds(i - K + ST);
       const float an_ = nr[r], ao = orr[r], fi = fr[r];
       const int kmax = EDGE ? min(S, n - 1 - i) : ST;
-      float num = an[r] + fi;  // j-side contributions so far + centre (w = 1)
-      float den = ad[r] + 1.f;
+      float num = an[r];  // centre + j-side contributions so far
+      float den = ad[r];
 #pragma unroll
       for (int k = 1; k <= ST; ++k) {
         const int rk = (r + k) % R;
@@ -202,8 +202,8 @@ __device__ __forceinline__ void walk_segment(const PassDesc& g, const float* __r
           orem = blk;
         }
       }
-      an[r] = 0.f;
-      ad[r] = 0.f;
+      an[r] = tf;  // pixel i + R enters slot r: centre term first
+      ad[r] = 1.f;
       lo = fminf(lo, tf);
       hi = fmaxf(hi, tf);
       fr[r] = tf;

@@ -311,12 +311,15 @@ __device__ __forceinline__ void walk2(const Pass2Desc& g, float* ring, const int
     fr[q] = ld(q + 1 + K);
     nr[q] = lds(q + 1 + 2 * K);
     orr[q] = lds(q);
-    an[q] = zero;
-    ad[q] = zero;
     d[q] = zero;
   }
+  const V one = Ops::splat(1.f);
 #pragma unroll
-  for (int q = 0; q < R; ++q) track(fr[q]);
+  for (int q = 0; q < R; ++q) {
+    track(fr[q]);
+    an[q] = fr[q];  // the centre sample (w = 1) starts each pixel's sums
+    ad[q] = one;
+  }
 #pragma unroll 1
   for (int t = 0; t <= 2 * K; ++t) {  // anchor d_k(i0-1), t ascending
     const V a = lds(t);
@@ -330,7 +333,6 @@ __device__ __forceinline__ void walk2(const Pass2Desc& g, float* ring, const int
 #pragma unroll 1
   for (int j = 0; j < 16; ++j) issue_piece(1, j);
 
-  const V one = Ops::splat(1.f);
   const int64_t dst_img = img * g.dst_img_stride;
   const int my_line = l0 + lane * LINES;
   float* op = g.dst + dst_img + (int64_t)my_line * g.dst_line_stride + (int64_t)s0 * g.dst_pos_stride;
@@ -368,8 +370,8 @@ __device__ __forceinline__ void walk2(const Pass2Desc& g, float* ring, const int
       const V to = lds(s + 1 + ST);
       const V an_ = nr[ra], ao = orr[ra], fi = fr[ra];
       const int kmax = EDGE ? min(S, n - 1 - i) : ST;
-      V num = Ops::add(an[ra], fi);
-      V den = Ops::add(ad[ra], one);
+      V num = an[ra];  // centre + j-side contributions so far
+      V den = ad[ra];
 #pragma unroll
       for (int k = 1; k <= ST; ++k) {
         const int rk = (ra + k) % R;
@@ -418,8 +420,8 @@ __device__ __forceinline__ void walk2(const Pass2Desc& g, float* ring, const int
           op += g.dst_pos_stride;
         }
       }
-      an[ra] = zero;
-      ad[ra] = zero;
+      an[ra] = tf;  // pixel i + R enters slot ra: centre term first
+      ad[ra] = one;
       track(tf);
       fr[ra] = tf;
       nr[ra] = tn;

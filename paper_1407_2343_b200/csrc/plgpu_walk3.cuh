@@ -243,7 +243,6 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
   const V zero = Ops::splat(0.f);
   const float sv = g.scale;
   auto sc = [&](V v) -> V { return Ops::scale(v, sv); };  // distance-side sample
-  const F2 zero2 = f2_make(0.f, 0.f);
   float lo0 = 3.402823466e38f, hi0 = -3.402823466e38f, lo1 = lo0, hi1 = hi0;
   auto track = [&](V v) {
     lo0 = fminf(lo0, Ops::lo(v));
@@ -257,13 +256,13 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
     orr[q] = sc(ld_init(q));
     d[q] = zero;
     const V f = ld_init(q + 1 + KT);
-    if constexpr (PK) {
+    if constexpr (PK) {  // the centre sample (w = 1) starts each pixel's sums
       frp[q] = f2_make(Ops::lo(f), 1.f);
-      acc[q] = zero2;
+      acc[q] = frp[q];
     } else {
       fr[q] = f;
-      an[q] = zero;
-      ad[q] = zero;
+      an[q] = f;
+      ad[q] = Ops::splat(1.f);
     }
     track(f);
   }
@@ -319,7 +318,7 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
         if constexpr (PK) {
           using O2 = VecOps<2>;
           const F2 fip = frp[r];
-          F2 nd = O2::add(acc[r], fip);  // {j-side num + f_i, j-side den + 1}
+          F2 nd = acc[r];  // {f_i + j-side num, 1 + j-side den}
 #pragma unroll
           for (int k = 1; k <= ST; ++k) {
             const int rk = (r + k) % R;
@@ -332,16 +331,17 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
             if constexpr (MASK) w = k > kmax ? 0.f : w;
             const F2 ww = f2_make(w, w);
             nd = O2::fma(frp[rk], ww, nd);  // num += w f_{i+k}; den += w
-            // first contribution to the slot recycled at step r-1: fma with 0
-            acc[rk] = O2::fma(fip, ww, k == ST ? zero2 : acc[rk]);
+            // first contribution to the slot recycled at step r-1: onto its
+            // centre term {f, 1}
+            acc[rk] = O2::fma(fip, ww, k == ST ? frp[rk] : acc[rk]);
           }
           float qn, qd;
           f2_split(nd, qn, qd);
           qv = div_fix(qn, qd);
         } else {
           const V fi = fr[r];
-          V num = Ops::add(an[r], fi);
-          V den = Ops::add(ad[r], one);
+          V num = an[r];  // centre + j-side contributions so far
+          V den = ad[r];
 #pragma unroll
           for (int k = 1; k <= ST; ++k) {
             const int rk = (r + k) % R;
@@ -354,9 +354,9 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
             if constexpr (MASK) w = Ops::zero_if(k > kmax, w);
             num = Ops::fma(w, fr[rk], num);
             den = Ops::add(w, den);
-            if (k == ST) {  // first contribution to the slot recycled at step r-1
-              an[rk] = Ops::fma(w, fi, zero);  // exactly the portable walker's fma(w, fi, 0)
-              ad[rk] = w;                      // == 0 + w (w >= +0)
+            if (k == ST) {  // first contribution to the slot recycled at step r-1,
+              an[rk] = Ops::fma(w, fi, fr[rk]);  // onto its centre term: the portable
+              ad[rk] = Ops::add(w, one);         // walker's fma(w, fi, f) and 1 + w
             } else {
               an[rk] = Ops::fma(w, fi, an[rk]);
               ad[rk] = Ops::add(w, ad[rk]);
