@@ -22,7 +22,8 @@
 //
 //     num[i] += w f[i+k]; den[i] += w;  num[i+k] += w f[i]; den[i+k] += w
 //
-// (WeightAccumulator, nlm.hpp:11-20; the centre sample weighs exactly 1).
+// (WeightAccumulator, nlm.hpp:11-20; the centre sample weighs exactly 1 and
+// seeds the pixel's sums when it enters the rings).
 // Nothing of the N x (2S+1) band is materialised: the samples live in three
 // register rings of S+1 (partners of the entering term, of the leaving term,
 // and the f values), the S distances in registers, and the pending
