@@ -338,8 +338,9 @@ def run_ours(args):
             pl.nlm_row_pass_blocked(x, params, cb, out=mid)
             torch.distributed.all_to_all_single(recv.reshape(-1), mid.reshape(-1))
         elif fused:
+            sym_barrier()  # peers done reading their windows (previous column pass)
             pl.nlm_row_pass_fanout(x[0], params, out=win[olo - wlo:ohi - wlo], extras=fan)
-            sym_barrier()
+            sym_barrier()  # every halo row delivered
         elif halo:
             pl.nlm_row_pass(x[0], params, out=win[olo - wlo:ohi - wlo])
             if p2p:

@@ -263,10 +263,12 @@ def halo_cols_fused(params, plan: HaloPlan, windows: Callable, *,
 
 def halo_rc_fused(x_rows, params, plan: HaloPlan, windows: Callable, barrier: Callable, *,
                   row_pass_fanout: Callable | None = None, col_pass_window: Callable | None = None):
-    """Row pass with fused halo stores -> barrier -> windowed column pass.
-    ``barrier()`` must order every rank's row pass (and its peer stores)
-    before any column pass, e.g. the symmetric-memory handle's device
-    barrier on the current stream."""
+    """barrier -> row pass with fused halo stores -> barrier -> windowed column
+    pass.  ``barrier()`` (e.g. the symmetric-memory handle's device barrier on
+    the current stream) orders every rank's row pass and its peer stores
+    before any column pass, and -- the first one -- every peer's previous
+    column pass (still reading its window) before this call's stores into it."""
+    barrier()
     halo_rows_fused(x_rows, params, plan, windows, row_pass_fanout=row_pass_fanout)
     barrier()
     return halo_cols_fused(params, plan, windows, col_pass_window=col_pass_window)
