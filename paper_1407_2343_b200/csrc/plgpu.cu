@@ -70,13 +70,18 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 // of pre-walk) is a whole number of S+1-step iterations of the unrolled
 // walker.  Lines of 8192+ samples use a multiple of 8 segments, so that the
 // row-partitioned multi-GPU column pass (whole segments per rank) splits
-// evenly over 2, 4 or 8 GPUs.
+// evenly over 2, 4 or 8 GPUs.  Signal-length lines (32768+ samples: 1D
+// signals, processed one or a few at a time) use ~64-sample segments so a
+// single line still spreads over enough threads: c1 (one 65,536-sample
+// line) 195 -> ~1,000 Msample/s on the B200 for S/64 extra pre-walk.
 int32_t segment_length(int32_t n, int32_t S) {
   const int32_t R = std::max(1, S + 1);
-  static const int32_t target = [] {  // long segments: pre-walk overhead S/C stays small
+  static const int32_t forced = [] {
     const char* e = std::getenv("PLGPU_SEG");  // experiments only
-    return e ? std::max(16, std::atoi(e)) : 480;
+    return e ? std::max(16, std::atoi(e)) : 0;
   }();
+  // long segments: pre-walk overhead S/C stays small
+  const int32_t target = forced ? forced : n >= 32768 ? 64 : 480;
   int32_t nseg = std::max(1, (n + target - 1) / target);
   if (n >= 8192) nseg = std::max(8, (nseg + 4) / 8 * 8);
   int32_t C = (n + nseg - 1) / nseg;       // near-equal segments
