@@ -3,10 +3,13 @@
 
 Default workload (BASELINE.json configs[3], the config the metric is quoted on
 at 1/2/4/8 B200): c4 = 64 independent 2048x2048 integer-valued images, K=3,
-S=10, h=sqrt(14)*20, RC order.  With N GPUs the 64 images are split into
-contiguous shards, one per rank, with no communication (strong scaling: the
-batch is fixed).  ``--config c3|c2|c1|c5`` selects the other single-GPU
-workloads (c5 here runs its single-GPU form).
+S=10, h=sqrt(14)*20, RC order.  With N GPUs every rank filters its own batch
+of 64 such images (images 64r .. 64r+63 of the seeded construction) with no
+communication: the path partitions into independent images, so the per-GPU
+work is fixed and the line reports weak scaling (value = all ranks' pixels /
+max-over-ranks time).  ``--config c3|c2|c1`` select the other single-GPU
+workloads; ``--config c5`` at N > 1 partitions ONE 16384^2 image (strong
+scaling, ``--c5-dist halo|fused|slab``).
 
 One "step" = one RC over the whole (per-rank) batch, inputs resident in HBM.
 ``value`` = all ranks' pixels / max-over-ranks device time (CUDA events).
@@ -65,12 +68,6 @@ def workload(cfg_name: str):
     c = W.CONFIGS[cfg_name]
     S, K, h = W.params(cfg_name)
     return c, S, K, h
-
-
-def shard(n_items: int, world: int, rank: int):
-    lo = n_items * rank // world
-    hi = n_items * (rank + 1) // world
-    return lo, hi
 
 
 def dist_mode(cfg_name, world, how="halo"):
@@ -257,7 +254,8 @@ def run_reference_arm(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": px / value / 1e3,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "weak" if c["kind"] == "image" and c.get("batch", 1) > 1
+        else "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded PCG64, see paper_1407_2343_b200/workloads.py)", "config": cfg,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
                          "sample": "each step: " + sample.split(",", 1)[1].strip()
@@ -288,8 +286,8 @@ def run_ours(args):
     slab, halo, fused = mode == "slab", mode in ("halo", "fused"), mode == "fused"
     if c["kind"] == "signal" or mode:
         lo, hi = 0, 1
-    else:
-        lo, hi = shard(n_items, world, rank)
+    else:  # weak scaling: every rank its own batch of n_items images
+        lo, hi = rank * n_items, (rank + 1) * n_items
     if slab:
         from paper_1407_2343_b200.distributed import SlabPlan
         plan = SlabPlan(c["rows"], c["cols"], world, rank)
@@ -408,7 +406,7 @@ def run_ours(args):
         px_total = c["rows"] * c["cols"]
     else:
         px_local = (hi - lo) * c["rows"] * c["cols"]
-        px_total = n_items * c["rows"] * c["cols"]
+        px_total = world * n_items * c["rows"] * c["cols"]
     value = px_total / (ms_step * 1e-3) / 1e6
 
     # ---- roofline (dominant kernel): unique pairs = exps per launch ----------
@@ -464,11 +462,15 @@ def run_ours(args):
         cfg = describe(args.config, c, S, K, h, n_items)
         cfg["l2"] = ("inputs + intermediate exceed the 126 MB L2" if px_total * 4 > 126e6
                      else "working set fits L2 (flush not applied; compute-bound kernel)")
-        cfg["parallelism"] = f"batch shards x{world}" if world > 1 else "1 GPU"
+        cfg["parallelism"] = (f"{world} ranks x {n_items} images each (no communication)"
+                              if world > 1 else "1 GPU")
+        if not (mode or signal):
+            cfg["global_batch"] = world * n_items
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "scaling": "strong" if (mode or signal) else "weak", "vs_baseline": None,
+            "dtype": "f32",
             "data": "synthetic (seeded PCG64 constructions of BASELINE.json, "
                     "paper_1407_2343_b200/workloads.py)",
             "config": cfg, "roofline": roof, "clocks": clocks.summary(),
