@@ -49,9 +49,11 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
-    ap.add_argument("--c5-dist", default="halo", choices=["halo", "fused", "slab"],
-                    help="c5 at N>1: row-partitioned halo exchange (default) or the "
-                         "row-slab -> all-to-all -> column-slab transpose")
+    ap.add_argument("--c5-dist", default="fused", choices=["fused", "halo", "slab"],
+                    help="c5 at N>1: row partition with the halo rows stored into the "
+                         "neighbours' symmetric-memory windows by the row-pass kernel (fused, "
+                         "default), the same with NCCL send/recv (halo), or the row-slab -> "
+                         "all-to-all -> column-slab transpose (slab)")
     return ap.parse_args()
 
 
