@@ -317,12 +317,22 @@ def run_ours(args):
         p2p = []
         if fused:
             from paper_1407_2343_b200.distributed import symmetric_windows
-            windows, sym_barrier = symmetric_windows(plan, dev)
-            win = windows(rank)[:whi - wlo]
-            fan = [(windows(d_)[row_:row_ + (hi_ - lo_)], lo_ - olo, hi_ - olo)
-                   for d_, lo_, hi_, row_ in plan.fanout()]
-            if len(fan) > pl.PL_MAX_FANOUT:
-                raise RuntimeError("fused halo: more than PL_MAX_FANOUT neighbours")
+            ok = torch.ones(1, device=dev)
+            try:
+                windows, sym_barrier = symmetric_windows(plan, dev)
+                fan = [(windows(d_)[row_:row_ + (hi_ - lo_)], lo_ - olo, hi_ - olo)
+                       for d_, lo_, hi_, row_ in plan.fanout()]
+                if len(fan) > pl.PL_MAX_FANOUT:
+                    raise RuntimeError("more than PL_MAX_FANOUT neighbours")
+            except Exception as e:  # no symmetric memory here: NCCL halo exchange instead
+                print(f"rank {rank}: fused halo unavailable ({e}); using NCCL send/recv",
+                      file=sys.stderr)
+                ok.zero_()
+            torch.distributed.all_reduce(ok, op=torch.distributed.ReduceOp.MIN)
+            if ok.item() > 0:
+                win = windows(rank)[:whi - wlo]
+            else:
+                fused = False
         for s_, d_, lo_, hi_ in ([] if fused else plan.transfers()):
             if s_ == rank:
                 p2p.append(torch.distributed.P2POp(torch.distributed.isend,
