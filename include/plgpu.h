@@ -24,7 +24,9 @@
  *  - Buffers are caller-owned device pointers (fp32 unless stated); images
  *    are batches of row-major [batch][rows][cols] planes.
  *  - Every call is stream-ordered on `stream` (a cudaStream_t, NULL = legacy
- *    default stream) and returns immediately; re-entrant per stream.
+ *    default stream) and returns immediately; re-entrant: concurrent calls on
+ *    different streams or host threads share no device state (library
+ *    scratch is allocated per call, stream-ordered, from a per-device pool).
  *  - Return value: PL_OK or an error code; the message of the last failure on
  *    the calling thread is pl_last_error().  Validation failures reuse the
  *    reference's exact ValidationError messages (core_types.cpp:13-77).
@@ -79,6 +81,10 @@ typedef struct pl_op_counts {
 
 int pl_abi_version(void);
 const char* pl_last_error(void);
+/* Diagnostic: the kernel route the last pass launched on the calling thread
+ * ("hot<S=..,K=..,lines=..,io=..,wpc=..,avg=..>", "staged<...>",
+ * "portable<...>", "direct", "none"); for composites, their last pass. */
+const char* pl_last_route(void);
 /* Name of the device the library will launch on, or "" if none. */
 const char* pl_device_name(void);
 
@@ -167,7 +173,9 @@ int pl_nlm_row_pass_fanout(const float* src, float* dst, int32_t rows, int32_t c
 size_t pl_workspace_bytes(int32_t op, int32_t batch, int32_t rows, int32_t cols);
 
 /* Composites.  `work` is caller-provided device scratch of
- * pl_workspace_bytes(...) bytes, or NULL to use a library-owned cache. */
+ * pl_workspace_bytes(...) bytes, or NULL: the call then allocates its own
+ * scratch on `stream` (cudaMallocFromPoolAsync from a per-device pool that
+ * keeps its memory) and frees it in stream order after its last kernel. */
 int pl_snlm_2d_row_col(const float* src, float* dst, float* work, int32_t batch, int32_t rows,
                        int32_t cols, pl_params p, void* stream);
 int pl_snlm_2d_col_row(const float* src, float* dst, float* work, int32_t batch, int32_t rows,
@@ -204,6 +212,17 @@ int pl_distance_band_f32(const float* src, float* band, int64_t n_lines, int32_t
  * filter and converts to int32. */
 int pl_distance_band_i32(const float* src, int32_t* band, int64_t n_lines, int32_t n, int64_t ld,
                          int32_t search_radius, int32_t patch_radius, void* stream);
+/* Debug: the distances the HOT filter kernel itself computes.  Runs the row
+ * pass of n_lines lines of n samples (row-major, ld = n) through the hot
+ * kernel's distance-export instantiation with the sample prescale set to 1,
+ * so its running-sum recurrence works on the raw samples, and stores every
+ * distance d(i, i+k) of the pixels it owns into band (layout as above, NaN
+ * elsewhere, diagonal cells not written).  Exact (bit-equal to the
+ * reference) on integer-valued inputs.  Needs n_lines >= 16 and a hot
+ * (K, S) pair: (3, 10), (5, 15), (7, 25), with S <= n - 1. */
+int pl_debug_hot_distance_band(const float* src, float* band, int32_t n_lines, int32_t n,
+                               int32_t search_radius, int32_t patch_radius, void* stream);
+
 /* F-bar cells of compute_banded_kernel in fp64, same diagonal recursion and
  * evaluation order as the reference (bit-equal to it). src is fp64. */
 int pl_banded_kernel_f64(const double* src, double* band, int64_t n_lines, int32_t n, int64_t ld,

@@ -288,7 +288,8 @@ class Reference(_Base):
         o4 = (C.c_uint64 * 4)()
         self._check(self.lib.ref_image_filter(C.c_int(FILTER_OPS[op]), _ptr(img), C.c_int(rows),
                                               C.c_int(cols), C.c_int(S), C.c_int(K), C.c_double(h),
-                                              C.c_int(threads), _ptr(out), C.cast(o4, _u64p)))
+                                              C.c_int(threads), _ptr(out),
+                                              C.cast(o4, _u64p) if ops is not None else None))
         if ops is not None:
             ops[:] = list(o4)
         return out

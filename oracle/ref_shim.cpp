@@ -140,14 +140,17 @@ int ref_image_filter(int op, const double* img, int rows, int cols, int S, int K
     const patchlift::Image2D in(rows, cols, std::vector<double>(img, img + cnt));
     const patchlift::NlmParams p{S, K, h};
     patchlift::OpCounter ops;
+    // no counter requested -> nullptr, as the reference's bench passes it
+    // (snlm_2d_row_col(img, p, nullptr, 0))
+    patchlift::OpCounter* po = ops4 ? &ops : nullptr;
     patchlift::Image2D r(1, 1);
     switch (op) {
-      case 0: r = patchlift::nlm_row_pass(in, p, &ops, threads); break;
-      case 1: r = patchlift::nlm_col_pass(in, p, &ops, threads); break;
-      case 2: r = patchlift::snlm_2d_row_col(in, p, &ops, threads); break;
-      case 3: r = patchlift::snlm_2d_col_row(in, p, &ops, threads); break;
-      case 4: r = patchlift::snlm_2d(in, p, &ops, threads); break;
-      case 5: r = patchlift::nlm_2d_naive(in, p, &ops, threads); break;
+      case 0: r = patchlift::nlm_row_pass(in, p, po, threads); break;
+      case 1: r = patchlift::nlm_col_pass(in, p, po, threads); break;
+      case 2: r = patchlift::snlm_2d_row_col(in, p, po, threads); break;
+      case 3: r = patchlift::snlm_2d_col_row(in, p, po, threads); break;
+      case 4: r = patchlift::snlm_2d(in, p, po, threads); break;
+      case 5: r = patchlift::nlm_2d_naive(in, p, po, threads); break;
       default: throw std::runtime_error("unknown filter op");
     }
     std::memcpy(out, r.data.data(), r.data.size() * sizeof(double));

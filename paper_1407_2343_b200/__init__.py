@@ -36,7 +36,8 @@ EXPORTS = [
     "pl_device_alloc", "pl_device_free", "pl_copy_to_device", "pl_copy_to_host",
     "pl_synchronize", "pl_distance_band_f32", "pl_distance_band_i32", "pl_banded_kernel_f64",
     "pl_col_window", "pl_nlm_col_pass_window", "pl_image_metrics_f32", "pl_image_metrics_f64",
-    "pl_nlm_pass_strided", "pl_nlm_row_pass_fanout",
+    "pl_nlm_pass_strided", "pl_nlm_row_pass_fanout", "pl_last_route",
+    "pl_debug_hot_distance_band",
 ]
 PL_MAX_FANOUT = 2
 
@@ -85,6 +86,8 @@ def lib() -> C.CDLL:
         sig = {
             "pl_abi_version": ([], C.c_int),
             "pl_last_error": ([], C.c_char_p),
+            "pl_last_route": ([], C.c_char_p),
+            "pl_debug_hot_distance_band": ([vp, vp, i32, i32, i32, i32, vp], C.c_int),
             "pl_device_name": ([], C.c_char_p),
             "pl_validate_params": ([P, i32], C.c_int),
             "pl_validate_geometry": ([i32, i32, i32], C.c_int),
@@ -159,6 +162,26 @@ def _dev(t, dtype=None):
     return t
 
 
+def _out(out, like, shape=None):
+    """A caller-supplied output: float32, contiguous, on like's device, with
+    exactly the expected number of elements (shape defaults to like's)."""
+    import torch
+    shape = tuple(like.shape) if shape is None else tuple(shape)
+    if out is None:
+        return torch.empty(shape, dtype=torch.float32, device=like.device)
+    _dev(out, torch.float32)
+    if out.device != like.device:
+        raise ValueError(f"out is on {out.device}, input on {like.device}")
+    if out.numel() != math.prod(shape):
+        raise ValueError(f"out has {out.numel()} elements, expected {math.prod(shape)} {shape}")
+    return out
+
+
+def last_route() -> str:
+    """Kernel route of the last pass launched on this thread (diagnostic)."""
+    return (lib().pl_last_route() or b"").decode()
+
+
 # ---------------------------------------------------------------------------
 # host-side helpers (no device)
 def validate_params(p, n: int) -> None:
@@ -204,7 +227,7 @@ def nlm_1d_patchlift(x, p, out=None):
     _dev(x, torch.float32)
     n = x.shape[-1]
     lines = x.numel() // n if n else 0
-    out = torch.empty_like(x) if out is None else out
+    out = _out(out, x)
     _check(lib().pl_nlm_lines(x.data_ptr(), out.data_ptr(), lines, n, n, _params(p), _stream(x)))
     return out
 
@@ -213,7 +236,7 @@ def nlm_1d_naive(x, p, out=None):
     import torch
     _dev(x, torch.float32)
     n = x.shape[-1]
-    out = torch.empty_like(x) if out is None else out
+    out = _out(out, x)
     _check(lib().pl_nlm_lines_naive(x.data_ptr(), out.data_ptr(), x.numel() // n, n, n,
                                     _params(p), _stream(x)))
     return out
@@ -223,7 +246,12 @@ def _image_op(name, x, p, out=None, work=None):
     import torch
     _dev(x, torch.float32)
     b, r, c = _image_dims(x)
-    out = torch.empty_like(x) if out is None else out
+    out = _out(out, x)
+    if work is not None:
+        _dev(work, torch.float32)
+        op = {"pl_snlm_2d_row_col": 0, "pl_snlm_2d_col_row": 1, "pl_snlm_2d": 2}[name]
+        if work.numel() * 4 < workspace_bytes(op, b, r, c) or work.device != x.device:
+            raise ValueError("work is smaller than pl_workspace_bytes or on another device")
     fn = getattr(lib(), name)
     if name in ("pl_nlm_row_pass", "pl_nlm_col_pass", "pl_nlm_2d_naive"):
         rc = fn(x.data_ptr(), out.data_ptr(), b, r, c, _params(p), _stream(x))
@@ -263,7 +291,7 @@ def nlm_row_pass_blocked(x, p, col_block: int, out=None):
     import torch
     _dev(x, torch.float32)
     b, r, c = _image_dims(x)
-    out = torch.empty_like(x) if out is None else out
+    out = _out(out, x)
     _check(lib().pl_nlm_row_pass_blocked(x.data_ptr(), out.data_ptr(), b, r, c, int(col_block),
                                          _params(p), _stream(x)))
     return out
@@ -282,7 +310,7 @@ def nlm_row_pass_fanout(x, p, out=None, extras=()):
     if x.dim() != 2:
         raise ValueError("expected one image [rows, cols]")
     r, c = x.shape
-    out = torch.empty_like(x) if out is None else out
+    out = _out(out, x)
     n = len(extras)
     ptrs = (C.c_void_p * max(1, n))(*[e[0] if isinstance(e[0], int) else e[0].data_ptr()
                                       for e in extras])
@@ -318,7 +346,7 @@ def nlm_col_pass_window(x_win, in_lo: int, rows_total: int, seg_begin: int, seg_
     b, r, c = _image_dims(x_win)
     _, _, out_lo, out_hi = col_window(rows_total, seg_begin, seg_end, p)
     shape = (out_hi - out_lo, c) if x_win.dim() == 2 else (b, out_hi - out_lo, c)
-    out = torch.empty(shape, dtype=torch.float32, device=x_win.device) if out is None else out
+    out = _out(out, x_win, shape)
     _check(lib().pl_nlm_col_pass_window(x_win.data_ptr(), int(in_lo), r, out.data_ptr(), b,
                                         int(rows_total), c, int(seg_begin), int(seg_end),
                                         _params(p), _stream(x_win)))
@@ -332,6 +360,15 @@ def nlm_pass_strided(src, dst, batch: int, lines: int, n: int, src_line_stride: 
     import torch
     _dev(src, torch.float32)
     _dev(dst, torch.float32)
+    if dst.device != src.device:
+        raise ValueError("src and dst on different devices")
+    # the last element each side addresses must lie inside the tensor
+    last_pos = int(batch - 1) * int(img_stride) + (int(n) - 1)
+    if (last_pos + (int(lines) - 1) * int(src_line_stride) + (int(n) - 1) * (int(src_pos_stride) - 1)
+            >= src.numel() or
+            last_pos + (int(lines) - 1) * int(dst_line_stride) + (int(n) - 1) * (int(dst_pos_stride) - 1)
+            >= dst.numel()):
+        raise ValueError("strides address past the end of src or dst")
     _check(lib().pl_nlm_pass_strided(src.data_ptr(), dst.data_ptr(), int(batch), int(lines), int(n),
                                      int(src_line_stride), int(src_pos_stride),
                                      int(dst_line_stride), int(dst_pos_stride), int(img_stride),
@@ -373,6 +410,19 @@ def distance_band(x, S: int, K: int, dtype=None):
     band = torch.empty((lines, n, 2 * S + 1), dtype=dtype, device=x.device)
     fn = lib().pl_distance_band_i32 if dtype == torch.int32 else lib().pl_distance_band_f32
     _check(fn(x.data_ptr(), band.data_ptr(), lines, n, n, int(S), int(K), _stream(x)))
+    return band
+
+
+def debug_hot_distance_band(x, S: int, K: int):
+    """Distances the HOT filter kernel computes (prescale 1) for the lines of
+    x ([lines, n], >= 16 lines, hot (K, S)): [lines, n, 2S+1] fp32, NaN where
+    not written (diagonal included).  Exact on integer-valued inputs."""
+    import torch
+    _dev(x, torch.float32)
+    lines, n = x.shape
+    band = torch.empty((lines, n, 2 * S + 1), dtype=torch.float32, device=x.device)
+    _check(lib().pl_debug_hot_distance_band(x.data_ptr(), band.data_ptr(), lines, n, int(S),
+                                            int(K), _stream(x)))
     return band
 
 

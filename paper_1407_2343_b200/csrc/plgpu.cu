@@ -21,6 +21,8 @@
 namespace {
 
 thread_local std::string g_err;
+// Diagnostic: which kernel route the last pass on this thread took.
+thread_local std::string g_route;
 
 int set_err(int code, const std::string& msg) {
   g_err = msg;
@@ -76,12 +78,8 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 // line) 195 -> ~1,000 Msample/s on the B200 for S/64 extra pre-walk.
 int32_t segment_length(int32_t n, int32_t S) {
   const int32_t R = std::max(1, S + 1);
-  static const int32_t forced = [] {
-    const char* e = std::getenv("PLGPU_SEG");  // experiments only
-    return e ? std::max(16, std::atoi(e)) : 0;
-  }();
   // long segments: pre-walk overhead S/C stays small
-  const int32_t target = forced ? forced : n >= 32768 ? 64 : 480;
+  const int32_t target = n >= 32768 ? 64 : 480;
   int32_t nseg = std::max(1, (n + target - 1) / target);
   if (n >= 8192) nseg = std::max(8, (nseg + 4) / 8 * 8);
   int32_t C = (n + nseg - 1) / nseg;       // near-equal segments
@@ -111,13 +109,6 @@ int walk3_lines(int ST) {
   if (ST > 16) return 1;
   if (forced) return forced;
   return ST <= 10 ? 2 : 1;  // measured on B200: c4 (S=10) 2 lines, c3 (S=15) 1 line
-}
-int walk3_minb() {
-  static const int v = [] {
-    const char* e = std::getenv("PLGPU_MINB");
-    return e ? std::atoi(e) : 1;
-  }();
-  return v;
 }
 int walk3_wpc(int ST) {
   static const int forced = [] {
@@ -150,6 +141,7 @@ int template_radius(int S) {
 }
 
 int dispatch_pass(const plgpu::PassDesc& g, cudaStream_t st) {
+  g_route = "portable<S=" + std::to_string(template_radius(g.S)) + ">";
   switch (template_radius(g.S)) {
 #define PL_CASE(v) \
   case v: plgpu::launch_pass<v>(g, st); break;
@@ -198,7 +190,7 @@ __global__ void direct_pass_kernel(plgpu::PassDesc g) {
 
 // Production walker launch, if the geometry qualifies (returns -1 if not).
 int try_pass2(const plgpu::PassDesc& g, cudaStream_t st) {
-  if (g.avg && g.src_pos_stride == 1) return -1;  // fused average: column-mode stores only
+  if (g.avg && g.dst_pos_stride == 1) return -1;  // fused average: column-mode flushes only
   // A warp carries 32-64 lines: for a handful of lines the one-thread-per-
   // segment portable walker wastes less.
   if (force_portable() || g.K > 7 || g.S < 1 || g.S > kMaxWalkS || g.lines_per_img < 16) return -1;
@@ -245,6 +237,7 @@ int try_pass2(const plgpu::PassDesc& g, cudaStream_t st) {
     d.xhi[x] = g.xhi[x];
   }
   d.avg = g.avg;
+  d.dexp = g.dexp;
   const int64_t images = g.n_lines / g.lines_per_img;
   d.total_warps = images * d.groups_per_img * d.nseg;
   const auto a16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
@@ -260,7 +253,6 @@ int try_pass2(const plgpu::PassDesc& g, cudaStream_t st) {
       d3.b = d;
       // lines per lane for the hot kernel (PLGPU_LINES=1|2 overrides)
       d3.lines = walk3_lines(ST);
-      d3.minb = walk3_minb();
       d3.wpc = walk3_wpc(ST);
       const int LW3 = 32 * d3.lines;
       d3.b.groups_per_img = (g.lines_per_img + LW3 - 1) / LW3;
@@ -299,9 +291,16 @@ int try_pass2(const plgpu::PassDesc& g, cudaStream_t st) {
         PLGPU_FOR_EACH_RADIUS(PL_CASE)
 #undef PL_CASE
       }
-      if (launched) return check_launch();
+      if (launched) {
+        g_route = "hot<S=" + std::to_string(ST) + ",K=" + std::to_string(KT3) + ",lines=" +
+                  std::to_string(d3.lines) + ",io=" + std::to_string(io) + ",wpc=" +
+                  std::to_string(d3.wpc) + ",avg=" + std::to_string(d.avg ? 1 : 0) + ">";
+        return check_launch();
+      }
     }
   }
+  g_route = "staged<S=" + std::to_string(ST) + ",rows=" + std::to_string(rows ? 1 : 0) + ">";
+  if (g.dexp) return set_err(PL_ERR_UNSUPPORTED, "distance export needs the hot kernel's (K, S)");
   switch (ST) {
 #define PL_CASE(v) \
   case v: plgpu::launch_pass2<v>(d, rows, st); break;
@@ -317,20 +316,24 @@ int run_pass(plgpu::PassDesc g, const pl_params& p, cudaStream_t st) {
   g.S = std::min<int32_t>(p.search_radius, g.n - 1);
   g.K = p.patch_radius;
   g.coef = weight_coef(p.h);
-  g.scale = static_cast<float>(std::sqrt(1.4426950408889634) / p.h);
+  // debug distance export: the recurrence on raw samples (exact on integers)
+  g.scale = g.dexp ? 1.0f : static_cast<float>(std::sqrt(1.4426950408889634) / p.h);
   g.seg_len = segment_length(g.n, g.S);
   if (g.nseg <= 0) {  // whole lines (windowed passes preset seg_begin / nseg)
     g.seg_begin = 0;
     g.nseg = (g.n + g.seg_len - 1) / g.seg_len;
   }
   if (g.dst_pos_block <= 0) g.dst_pos_block = g.n;
+  g_route = "none";
   if (g.n_lines <= 0) return PL_OK;
   if (g.n_lines % g.lines_per_img == 0) {
     const int rc = try_pass2(g, st);
     if (rc >= 0) return rc;
   }
+  if (g.dexp) return set_err(PL_ERR_UNSUPPORTED, "distance export needs the hot kernel");
   if (g.S >= 1 && g.S <= kMaxWalkS) return dispatch_pass(g, st);
   const int64_t work = g.n_lines * g.n;
+  g_route = "direct";
   direct_pass_kernel<<<(unsigned)((work + 127) / 128), 128, 0, st>>>(g);
   return check_launch();
 }
@@ -385,32 +388,57 @@ int rc_passes(const float* src, float* dst, float* mid, int batch, int rows, int
   return run_pass(b, p, st);
 }
 
-// Library-owned workspace cache (per device, grown on demand, stream-ordered use).
-struct Workspace {
-  std::mutex mu;
-  void* ptr = nullptr;
-  size_t bytes = 0;
-};
-Workspace g_ws[64];
+// Library-owned scratch (work = NULL): stream-ordered allocations from one
+// memory pool per device (cudaMallocFromPoolAsync / cudaFreeAsync on the
+// caller's stream).  Every call gets its own buffer, released in stream order
+// after its last kernel, so concurrent calls on different streams (or host
+// threads) never share an intermediate, and nothing is freed while a caller
+// may still use it.  The pool keeps its memory (release threshold = max), so a
+// steady stream of calls does not go back to the driver.
+std::mutex g_pool_mu;
+cudaMemPool_t g_pool[64] = {};
 
-int get_workspace(size_t bytes, float** out) {
+int device_pool(cudaMemPool_t* out) {
   int dev = 0;
   PL_CUDA(cudaGetDevice(&dev));
-  Workspace& ws = g_ws[dev & 63];
-  std::lock_guard<std::mutex> lk(ws.mu);
-  if (ws.bytes < bytes) {
-    if (ws.ptr) {
-      PL_CUDA(cudaDeviceSynchronize());
-      PL_CUDA(cudaFree(ws.ptr));
-      ws.ptr = nullptr;
-      ws.bytes = 0;
-    }
-    PL_CUDA(cudaMalloc(&ws.ptr, bytes));
-    ws.bytes = bytes;
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  cudaMemPool_t& pool = g_pool[dev & 63];
+  if (!pool) {
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    PL_CUDA(cudaMemPoolCreate(&pool, &props));
+    uint64_t keep = UINT64_MAX;
+    PL_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
   }
-  *out = static_cast<float*>(ws.ptr);
+  *out = pool;
   return PL_OK;
 }
+
+// Scratch owned by one call: allocated on `st`, freed on `st` when the
+// object goes out of scope (after the call has enqueued its kernels).
+class Scratch {
+ public:
+  explicit Scratch(cudaStream_t st) : st_(st) {}
+  ~Scratch() {
+    if (ptr_) cudaFreeAsync(ptr_, st_);
+  }
+  Scratch(const Scratch&) = delete;
+  Scratch& operator=(const Scratch&) = delete;
+  int alloc(size_t bytes, float** out) {
+    cudaMemPool_t pool;
+    int rc = device_pool(&pool);
+    if (rc) return rc;
+    PL_CUDA(cudaMallocFromPoolAsync(&ptr_, bytes ? bytes : 16, pool, st_));
+    *out = static_cast<float*>(ptr_);
+    return PL_OK;
+  }
+
+ private:
+  cudaStream_t st_;
+  void* ptr_ = nullptr;
+};
 
 int check_ptrs(const void* a, const void* b) {
   if (!a || !b) return set_err(PL_ERR_ARG, "null buffer");
@@ -462,6 +490,8 @@ extern "C" {
 int pl_abi_version(void) { return PLGPU_ABI_VERSION; }
 
 const char* pl_last_error(void) { return g_err.c_str(); }
+
+const char* pl_last_route(void) { return g_route.c_str(); }
 
 const char* pl_device_name(void) {
   static thread_local char name[256];
@@ -717,7 +747,8 @@ int pl_snlm_2d_row_col(const float* src, float* dst, float* work, int32_t batch,
   if (!rc) rc = validate_params(p, cols);
   if (!rc) rc = check_ptrs(src, dst);
   if (rc) return rc;
-  if (!work && (rc = get_workspace(pl_workspace_bytes(0, batch, rows, cols), &work))) return rc;
+  Scratch scratch(as_stream(stream));
+  if (!work && (rc = scratch.alloc(pl_workspace_bytes(0, batch, rows, cols), &work))) return rc;
   return rc_passes(src, dst, work, batch, rows, cols, p, as_stream(stream));
 }
 
@@ -728,8 +759,9 @@ int pl_snlm_2d_col_row(const float* src, float* dst, float* work, int32_t batch,
   if (!rc) rc = validate_params(p, cols);
   if (!rc) rc = check_ptrs(src, dst);
   if (rc) return rc;
-  if (!work && (rc = get_workspace(pl_workspace_bytes(1, batch, rows, cols), &work))) return rc;
   cudaStream_t st = as_stream(stream);
+  Scratch scratch(st);
+  if (!work && (rc = scratch.alloc(pl_workspace_bytes(1, batch, rows, cols), &work))) return rc;
   if ((rc = run_pass(col_desc(src, work, batch, rows, cols), p, st))) return rc;
   return run_pass(row_desc(work, dst, batch, rows, cols), p, st);
 }
@@ -741,7 +773,8 @@ int pl_snlm_2d(const float* src, float* dst, float* work, int32_t batch, int32_t
   if (!rc) rc = validate_params(p, cols);
   if (!rc) rc = check_ptrs(src, dst);
   if (rc) return rc;
-  if (!work && (rc = get_workspace(pl_workspace_bytes(2, batch, rows, cols), &work))) return rc;
+  Scratch scratch(as_stream(stream));
+  if (!work && (rc = scratch.alloc(pl_workspace_bytes(2, batch, rows, cols), &work))) return rc;
   const int64_t cnt = (int64_t)batch * rows * cols;
   float* cr_img = work;
   float* mid = work + cnt;
@@ -762,64 +795,91 @@ int pl_snlm_2d_row_col_host(const float* host_src, float* host_dst, int32_t batc
   // copy-out (D2H engine) on three streams ordered by events, NSLOT device
   // slots of (in, mid, out) so image b+2's upload, image b+1's filter and
   // image b's download run concurrently.  Group images so each transfer is
-  // >= ~8 MiB (fewer, larger copies).
+  // >= ~8 MiB (fewer, larger copies).  Every CUDA call is checked; on an
+  // error the pipeline drains (all three streams synchronised) before the
+  // first error is returned.
   cudaStream_t st = as_stream(stream);
   const size_t img = (size_t)rows * cols;
   const int per = (int)std::max<size_t>(1, std::min<size_t>(batch, (8u << 20) / (img * 4) + 1));
   const int ngroups = (batch + per - 1) / per;
   constexpr int NSLOT = 3;
   const size_t slot_elems = 3 * img * per;
+  struct Pipe {
+    cudaStream_t s_in = nullptr, s_out = nullptr;
+    cudaEvent_t ev[3 * NSLOT + 2] = {};
+    ~Pipe() {
+      for (cudaEvent_t e : ev)
+        if (e) cudaEventDestroy(e);
+      if (s_in) cudaStreamDestroy(s_in);
+      if (s_out) cudaStreamDestroy(s_out);
+    }
+  } pipe;
+  PL_CUDA(cudaStreamCreateWithFlags(&pipe.s_in, cudaStreamNonBlocking));
+  PL_CUDA(cudaStreamCreateWithFlags(&pipe.s_out, cudaStreamNonBlocking));
+  for (cudaEvent_t& e : pipe.ev) PL_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  cudaEvent_t* up = pipe.ev;
+  cudaEvent_t* done = pipe.ev + NSLOT;
+  cudaEvent_t* freed = pipe.ev + 2 * NSLOT;
+  cudaEvent_t start = pipe.ev[3 * NSLOT], drained = pipe.ev[3 * NSLOT + 1];
+  Scratch scratch(st);  // freed on st after `drained` (below)
   float* buf = nullptr;
-  if ((rc = get_workspace(NSLOT * slot_elems * sizeof(float), &buf))) return rc;
-  cudaStream_t s_in = nullptr, s_out = nullptr;
-  PL_CUDA(cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking));
-  PL_CUDA(cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking));
-  cudaEvent_t up[NSLOT], done[NSLOT], freed[NSLOT];
-  for (int k = 0; k < NSLOT; ++k) {
-    cudaEventCreateWithFlags(&up[k], cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&done[k], cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&freed[k], cudaEventDisableTiming);
-  }
-  // the caller's stream orders the whole pipeline after prior work
-  cudaEvent_t start;
-  cudaEventCreateWithFlags(&start, cudaEventDisableTiming);
-  cudaEventRecord(start, st);
-  cudaStreamWaitEvent(s_in, start, 0);
-  for (int gi = 0; gi < ngroups && !rc; ++gi) {
+  if ((rc = scratch.alloc(NSLOT * slot_elems * sizeof(float), &buf))) return rc;
+  // the caller's stream orders the whole pipeline after prior work (and the allocation)
+  PL_CUDA(cudaEventRecord(start, st));
+  PL_CUDA(cudaStreamWaitEvent(pipe.s_in, start, 0));
+  auto step = [&](int gi) -> int {
     const int k = gi % NSLOT;
     const int b0 = gi * per, nb = std::min(per, batch - b0);
     float* in = buf + k * slot_elems;
     float* mid = in + img * per;
     float* out = mid + img * per;
-    if (gi >= NSLOT) cudaStreamWaitEvent(s_in, freed[k], 0);  // slot's previous download done
-    cudaMemcpyAsync(in, host_src + (size_t)b0 * img, nb * img * sizeof(float),
-                    cudaMemcpyHostToDevice, s_in);
-    cudaEventRecord(up[k], s_in);
-    cudaStreamWaitEvent(st, up[k], 0);
-    if ((rc = rc_passes(in, out, mid, nb, rows, cols, p, st))) break;
-    cudaEventRecord(done[k], st);
-    cudaStreamWaitEvent(s_out, done[k], 0);
-    cudaMemcpyAsync(host_dst + (size_t)b0 * img, out, nb * img * sizeof(float),
-                    cudaMemcpyDeviceToHost, s_out);
-    cudaEventRecord(freed[k], s_out);
-  }
-  cudaError_t e1 = cudaStreamSynchronize(s_out);
-  cudaError_t e2 = cudaStreamSynchronize(s_in);
-  cudaError_t e3 = cudaStreamSynchronize(st);
-  for (int k = 0; k < NSLOT; ++k) {
-    cudaEventDestroy(up[k]);
-    cudaEventDestroy(done[k]);
-    cudaEventDestroy(freed[k]);
-  }
-  cudaEventDestroy(start);
-  cudaStreamDestroy(s_in);
-  cudaStreamDestroy(s_out);
+    if (gi >= NSLOT) PL_CUDA(cudaStreamWaitEvent(pipe.s_in, freed[k], 0));  // slot's download done
+    PL_CUDA(cudaMemcpyAsync(in, host_src + (size_t)b0 * img, nb * img * sizeof(float),
+                            cudaMemcpyHostToDevice, pipe.s_in));
+    PL_CUDA(cudaEventRecord(up[k], pipe.s_in));
+    PL_CUDA(cudaStreamWaitEvent(st, up[k], 0));
+    int r = rc_passes(in, out, mid, nb, rows, cols, p, st);
+    if (r) return r;
+    PL_CUDA(cudaEventRecord(done[k], st));
+    PL_CUDA(cudaStreamWaitEvent(pipe.s_out, done[k], 0));
+    PL_CUDA(cudaMemcpyAsync(host_dst + (size_t)b0 * img, out, nb * img * sizeof(float),
+                            cudaMemcpyDeviceToHost, pipe.s_out));
+    PL_CUDA(cudaEventRecord(freed[k], pipe.s_out));
+    return PL_OK;
+  };
+  for (int gi = 0; gi < ngroups && !rc; ++gi) rc = step(gi);
+  // the scratch is released on st only after the last download
+  cudaError_t e0 = cudaEventRecord(drained, pipe.s_out);
+  if (e0 == cudaSuccess) e0 = cudaStreamWaitEvent(st, drained, 0);
+  const cudaError_t e1 = cudaStreamSynchronize(pipe.s_out);
+  const cudaError_t e2 = cudaStreamSynchronize(pipe.s_in);
+  const cudaError_t e3 = cudaStreamSynchronize(st);
   if (rc) return rc;
-  const cudaError_t e = e1 != cudaSuccess ? e1 : (e2 != cudaSuccess ? e2 : e3);
-  if (e != cudaSuccess) return set_err(PL_ERR_CUDA, std::string("host pipeline: ") + cudaGetErrorString(e));
+  for (cudaError_t e : {e0, e1, e2, e3})
+    if (e != cudaSuccess) return set_err(PL_ERR_CUDA, std::string("host pipeline: ") + cudaGetErrorString(e));
   return check_launch();
 }
 
+
+int pl_debug_hot_distance_band(const float* src, float* band, int32_t n_lines, int32_t n,
+                               int32_t S, int32_t K, void* stream) {
+  int rc = validate_image(1, n_lines, n);
+  if (!rc) rc = validate_geometry(S, K, n);
+  if (!rc) rc = check_ptrs(src, band);
+  if (rc) return rc;
+  if (n_lines < 16 || S > n - 1 || plgpu::pass3_k_for(template_radius(S)) != K ||
+      template_radius(S) != S)
+    return set_err(PL_ERR_UNSUPPORTED,
+                   "hot distance export needs >= 16 lines, a hot (K, S) pair and S <= n - 1");
+  cudaStream_t st = as_stream(stream);
+  PL_CUDA(cudaMemsetAsync(band, 0xFF, sizeof(float) * (size_t)n_lines * n * (2 * S + 1), st));
+  Scratch scratch(st);
+  float* out = nullptr;
+  if ((rc = scratch.alloc(sizeof(float) * (size_t)n_lines * n, &out))) return rc;
+  plgpu::PassDesc g = row_desc(src, out, 1, n_lines, n);
+  g.dexp = band;
+  return run_pass(g, pl_params{S, K, 1.0}, st);
+}
 
 int pl_distance_band_f32(const float* src, float* band, int64_t n_lines, int32_t n, int64_t ld,
                          int32_t S, int32_t K, void* stream) {

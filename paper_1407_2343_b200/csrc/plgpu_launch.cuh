@@ -69,7 +69,7 @@ void launch_pass2(const Pass2Desc& g, bool rows, cudaStream_t st) {
   launch_pass2_k<ST, -1>(g, rows, st);  // runtime K (K <= 7)
 }
 
-template <int ST, int KT, int L, int IO, int WPC, bool AVG>
+template <int ST, int KT, int L, int IO, int WPC, bool AVG, bool EXP = false>
 void launch3(const Pass3Desc& d, cudaStream_t st) {
   const size_t smem = sizeof(float) * WPC * pass3_smem_floats_per_warp<ST, L, IO>();
   unsigned grid;
@@ -80,7 +80,7 @@ void launch3(const Pass3Desc& d, cudaStream_t st) {
   } else {
     grid = (unsigned)((d.b.total_warps + WPC - 1) / WPC);
   }
-  auto k = nlm_pass3_kernel<ST, KT, L, IO, WPC, AVG>;
+  auto k = nlm_pass3_kernel<ST, KT, L, IO, WPC, AVG, EXP>;
   if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k<<<grid, 32 * WPC, smem, st>>>(d);
 }
@@ -92,10 +92,15 @@ bool launch_pass3(const Pass3Desc& d, int io, cudaStream_t st) {
     return false;
   } else {
     if (d.b.K != KT || d.b.S != ST) return false;
+    if (d.b.dexp && io != 1) return false;
     constexpr int DW = pass3_default_wpc(ST);
     // (register-capped variants, minb 6/8, measured slower on B200: profiles/README.md)
     auto go = [&](auto lines_tag) {
       constexpr int L = decltype(lines_tag)::value;
+      if (d.b.dexp) {  // debug distance export (row pass only, checked below)
+        launch3<ST, KT, L, 1, DW, false, true>(d, st);
+        return;
+      }
       if (io == 1) {
         if (d.wpc == 8) launch3<ST, KT, L, 1, 8, false>(d, st);
         else launch3<ST, KT, L, 1, 2, false>(d, st);

@@ -71,6 +71,9 @@ struct PassDesc {
   float* xdst[2];
   int32_t xlo[2], xhi[2];
   int32_t nx;
+  // Debug (pl_debug_hot_distance_band): the hot kernel also stores every
+  // distance it computes into this band ([line][n][2S+1]); NULL otherwise.
+  float* dexp;
 };
 
 __device__ __forceinline__ float ex2_approx(float x) {

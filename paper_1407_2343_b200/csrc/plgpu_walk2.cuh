@@ -197,6 +197,7 @@ struct Pass2Desc {
   float* xdst[2];
   int32_t xlo[2], xhi[2];
   int32_t nx;
+  float* dexp;  // debug distance export (hot kernel only, see PassDesc)
 };
 
 constexpr int kCH = 16;  // positions per chunk

@@ -60,7 +60,6 @@ __host__ __device__ constexpr int pass3_smem_floats_per_warp() {
 struct Pass3Desc {
   Pass2Desc b;          // geometry (strides, lines, segments, coef, S, K)
   int32_t lines;        // lines per lane (1 or 2); b.total_warps / groups follow it
-  int32_t minb;         // unused (register-cap experiments)
   int32_t wpc;          // warps per CTA: 2 (independent) or 8 (lockstep)
   int32_t seg_lo, seg_hi;  // segments (relative to b.seg_begin) needing no clipping (S > 16)
   int64_t interior_warps;  // groups * (seg_hi - seg_lo + 1)
@@ -78,7 +77,11 @@ __host__ __device__ constexpr bool pass3_split(int ST) { return ST > 16; }  // S
 // 1 = row staging + row flush (positions contiguous on both sides);
 // 2 = row staging + column flush (positions contiguous in the source, lines
 // contiguous in the destination: the transposed-intermediate RC composite).
-template <int ST, int KT, int LINES, int IO, int MODE = 0, bool AVG = false>
+// EXP (debug instantiation, pl_debug_hot_distance_band): every distance the
+// walk computes for a pixel of this segment is also stored into g.dexp, so
+// the exactness of the code that actually runs can be checked (with the
+// prescale set to 1 the recurrence runs on the raw samples).
+template <int ST, int KT, int LINES, int IO, int MODE = 0, bool AVG = false, bool EXP = false>
 __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int lane,
                                       const int64_t grp, const int seg, const int bar_threads = 0) {
   constexpr bool ROWS = IO != 0;   // transposing (row-mode) staging
@@ -279,6 +282,21 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
   const V one = Ops::splat(1.f);
   const int64_t dst_img = img * g.dst_img_stride;
   const int my_line = l0 + lane * LINES;
+  // debug distance export: pair (i, i+k) into cells (i, S+k) and (i+k, S-k)
+  auto dexport = [&](int i, int k, int kmax, V dk) {
+    if constexpr (EXP) {
+      if (i < s0 || i >= s1 || k > kmax) return;
+      const int64_t W = 2 * S + 1;
+#pragma unroll
+      for (int h = 0; h < LINES; ++h) {
+        if (my_line + h > last_line) continue;
+        float* b = g.dexp + ((int64_t)img * g.lines_per_img + my_line + h) * n * W;
+        const float v = h == 0 ? Ops::lo(dk) : Ops::hi(dk);
+        b[(int64_t)i * W + S + k] = v;
+        b[(int64_t)(i + k) * W + S - k] = v;
+      }
+    }
+  };
 
   // One chunk iteration (staging, R-step body, flush).  Clean iterations
   // (no masking) form a prefix of the loop and run in a loop of their own, so
@@ -327,6 +345,7 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
             const float dq = ao - orr[rk];
             dk = fmaf(-dq, dq, dk);
             d[k] = dk;
+            dexport(i, k, MASK ? kmax : min(S, n - 1 - i), dk);
             float w = ex2_approx(-dk);
             if constexpr (MASK) w = k > kmax ? 0.f : w;
             const F2 ww = f2_make(w, w);
@@ -350,6 +369,7 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
             const V dq = Ops::sub(ao, orr[rk]);
             dk = Ops::fms(dq, dq, dk);
             d[k] = dk;
+            dexport(i, k, MASK ? kmax : min(S, n - 1 - i), dk);
             V w = Ops::ex2n(dk);
             if constexpr (MASK) w = Ops::zero_if(k > kmax, w);
             num = Ops::fma(w, fr[rk], num);
@@ -535,7 +555,8 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
 // WPC = warps per CTA.  WPC = 2: independent warps.  WPC = 8 ("lockstep"):
 // the CTA's warps take 8 consecutive line groups of ONE segment and
 // synchronise once per iteration (named barrier over the active warps).
-template <int ST, int KT, int LINES, int IO, int WPC = kWarpsPerCta, bool AVG = false>
+template <int ST, int KT, int LINES, int IO, int WPC = kWarpsPerCta, bool AVG = false,
+          bool EXP = false>
 __global__ void __launch_bounds__(32 * WPC, 1)
     nlm_pass3_kernel(const Pass3Desc d) {
   extern __shared__ __align__(16) float smem[];
@@ -571,30 +592,30 @@ __global__ void __launch_bounds__(32 * WPC, 1)
     const int64_t grp = img * g.groups_per_img + gb + wib;
     const int bt = active * 32;
     if constexpr (!pass3_split(ST)) {
-      walk3<ST, KT, LINES, IO, 0, AVG>(g, ring, lane, grp, seg, bt);
+      walk3<ST, KT, LINES, IO, 0, AVG, EXP>(g, ring, lane, grp, seg, bt);
     } else if (interior) {
-      walk3<ST, KT, LINES, IO, 1, AVG>(g, ring, lane, grp, seg, bt);
+      walk3<ST, KT, LINES, IO, 1, AVG, EXP>(g, ring, lane, grp, seg, bt);
     } else {
-      walk3<ST, KT, LINES, IO, 2, AVG>(g, ring, lane, grp, seg, bt);
+      walk3<ST, KT, LINES, IO, 2, AVG, EXP>(g, ring, lane, grp, seg, bt);
     }
     return;
   }
   const int64_t wid = (int64_t)blockIdx.x * WPC + wib;
   if (wid >= g.total_warps) return;
   if constexpr (!pass3_split(ST)) {
-    walk3<ST, KT, LINES, IO, 0, AVG>(g, ring, lane, wid / g.nseg, g.seg_begin + (int)(wid % g.nseg));
+    walk3<ST, KT, LINES, IO, 0, AVG, EXP>(g, ring, lane, wid / g.nseg, g.seg_begin + (int)(wid % g.nseg));
   } else {
     // large S: interior warps (segments needing no clipping) first, then edges
     const int n_int = max(0, d.seg_hi - d.seg_lo + 1);
     if (wid < d.interior_warps) {
-      walk3<ST, KT, LINES, IO, 1, AVG>(g, ring, lane, wid / n_int,
+      walk3<ST, KT, LINES, IO, 1, AVG, EXP>(g, ring, lane, wid / n_int,
                                      g.seg_begin + d.seg_lo + (int)(wid % n_int));
     } else {
       const int n_edge = g.nseg - n_int;
       const int64_t e = wid - d.interior_warps;
       int sidx = (int)(e % n_edge);
       if (n_int > 0 && sidx >= d.seg_lo) sidx += n_int;
-      walk3<ST, KT, LINES, IO, 2, AVG>(g, ring, lane, e / n_edge, g.seg_begin + sidx);
+      walk3<ST, KT, LINES, IO, 2, AVG, EXP>(g, ring, lane, e / n_edge, g.seg_begin + sidx);
     }
   }
 }

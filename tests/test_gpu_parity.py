@@ -421,7 +421,8 @@ def test_portable_and_production_walkers_bitwise_equal(tmp_path):
         "outs = {}\n"
         "for (b, r, c, S, K) in [(2, 300, 517, 10, 3), (1, 260, 700, 15, 5), (1, 333, 290, 25, 7),"
         " (3, 64, 128, 4, 2), (1, 40, 1000, 32, 7), (2, 1100, 96, 10, 3), (1, 70, 1500, 15, 5),"
-        " (1, 900, 100, 25, 7), (1, 7, 3000, 10, 3)]:\n"
+        " (1, 900, 100, 25, 7), (1, 7, 3000, 10, 3), (1, 40, 9000, 25, 7), (1, 1700, 64, 25, 7),"
+        " (1, 64, 2000, 15, 5), (1, 1600, 96, 15, 5), (1, 33, 16384, 25, 7)]:\n"
         "    x = torch.from_numpy(rng.uniform(0, 255, (b, r, c)).astype(np.float32)).cuda()\n"
         "    p = (S, K, 50.0 + 10 * S)\n"
         "    outs[f'{r}x{c}_rc'] = pl.snlm_2d_row_col(x, p).cpu().numpy()\n"

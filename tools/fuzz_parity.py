@@ -33,6 +33,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--seconds", type=float, default=120)
     ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--long-frac", type=float, default=0.15,
+                    help="fraction of cases with one 1,500-20,000-sample axis")
     a = ap.parse_args()
     rng = np.random.default_rng(a.seed)
     orc = Oracle.get()
@@ -45,6 +47,10 @@ def main():
             S, K = int(rng.integers(0, 33)), int(rng.integers(0, 9))
         b = int(rng.integers(1, 4))
         r, c = int(rng.integers(1, 420)), int(rng.integers(1, 420))
+        if rng.uniform() < a.long_frac:  # long lines: interior segments of the hot kernel
+            b = 1
+            long_n, short_n = int(rng.integers(1500, 20000)), int(rng.integers(1, 100))
+            r, c = (long_n, short_n) if rng.uniform() < 0.5 else (short_n, long_n)
         if K > min(r, c):
             continue
         kind = rng.integers(0, 4)
