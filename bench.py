@@ -2,17 +2,21 @@
 """Benchmark of the separable PatchLift-NLM hot path (row pass -> column pass).
 
 Default workload (BASELINE.json configs[3], the config the metric is quoted on
-at 1/2/4/8 B200): c4 = 64 independent 2048x2048 integer-valued images, K=3,
-S=10, h=sqrt(14)*20, RC order.  With N GPUs every rank filters its own batch
-of 64 such images (images 64r .. 64r+63 of the seeded construction) with no
-communication: the path partitions into independent images, so the per-GPU
-work is fixed and the line reports weak scaling (value = all ranks' pixels /
-max-over-ranks time).  ``--config c3|c2|c1`` select the other single-GPU
-workloads; ``--config c5`` at N > 1 partitions ONE 16384^2 image (strong
-scaling, ``--c5-dist halo|fused|slab``).
+at 1/2/4/8 B200): c4 = a batch of 64 independent 2048x2048 integer-valued
+images, K=3, S=10, h=sqrt(14)*20, RC order.  With N GPUs the 64 images are
+sharded contiguously over the ranks with no communication (BASELINE's config,
+"scaling": "strong"); the same line carries the weak form (every rank its own
+64 images) and, at N > 1, the north-star single-image config c5 in all three
+partition forms (slab all-to-all, NCCL halo, fused NVLink halo), each checked
+bitwise against the single-GPU RC.  ``--config c3|c2|c1`` select the other
+single-GPU workloads; ``--config c5`` at N > 1 makes the c5 form chosen by
+``--c5-dist`` (default slab) the line.
 
 One "step" = one RC over the whole (per-rank) batch, inputs resident in HBM.
 ``value`` = all ranks' pixels / max-over-ranks device time (CUDA events).
+``roofline.frac`` = unique pairs per launch of the dominant pass kernel / its
+event time, over the NOMINAL 16 EX2 per clock per SM (BASELINE.md sec. 4);
+``frac_measured_peak`` uses this GPU's live MUFU / FP32 microbenchmarks.
 ``e2e`` = the same metric through the C-ABI host entry point
 (pl_snlm_2d_row_col_host) with pinned host buffers, H2D + D2H inside.
 ``--impl reference`` times the reference's own CPU implementation
@@ -49,11 +53,17 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
-    ap.add_argument("--c5-dist", default="fused", choices=["fused", "halo", "slab"],
-                    help="c5 at N>1: row partition with the halo rows stored into the "
-                         "neighbours' symmetric-memory windows by the row-pass kernel (fused, "
-                         "default), the same with NCCL send/recv (halo), or the row-slab -> "
-                         "all-to-all -> column-slab transpose (slab)")
+    ap.add_argument("--c5-dist", default="slab", choices=["slab", "halo", "fused"],
+                    help="c5 at N>1: row slabs -> NCCL all-to-all -> column slabs (slab, the "
+                         "north-star design, default), row partition + NCCL halo send/recv "
+                         "(halo), or the same partition with the halo rows stored into the "
+                         "neighbours' symmetric-memory windows by the row-pass kernel (fused); "
+                         "the other two forms are reported as fields of the same line")
+    ap.add_argument("--no-c5-forms", action="store_true",
+                    help="default c4 run at N>1: skip the c5 forms riding along")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: functional check of the N>1 logic with every rank on cuda:0 "
+                         "(timings meaningless)")
     return ap.parse_args()
 
 
@@ -236,8 +246,7 @@ def cpu_reference_rate(cfg_name, imgs_host, S, K, h, seconds, max_items=None):
 def run_reference_arm(args):
     world, rank, local = dist_env()
     c, S, K, h = workload(args.config)
-    n_items = c.get("batch", 1)
-    cfg = describe(args.config, c, S, K, h, n_items)
+    cfg = arm_config(args.config, world)
     if rank != 0:
         return
     sample_imgs = make_inputs(args.config, 0, 1)
@@ -256,12 +265,14 @@ def run_reference_arm(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": px / value / 1e3,
-        "higher_is_better": True, "scaling": "weak" if c["kind"] == "image" and c.get("batch", 1) > 1
-        else "strong", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded PCG64, see paper_1407_2343_b200/workloads.py)", "config": cfg,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
                          "sample": "each step: " + sample.split(",", 1)[1].strip()
-                         if "," in sample else sample},
+                         if "," in sample else sample,
+                         "images_per_step": 1, "cpu_model": cpu_model()},
+        "sample": "a bounded sample of the workload: each step filters ONE of its images "
+                  "(Mpixel/s is per pixel, so the rate compares with the full batch)",
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "wall_s": wall,
     }
@@ -269,126 +280,138 @@ def run_reference_arm(args):
 
 
 # --------------------------------------------------------------------------- ours
-def run_ours(args):
-    import torch
-    import paper_1407_2343_b200 as pl
+class Dist:
+    """Process-group plumbing.  ``nccl`` (the product: one rank per GPU) or
+    ``gloo`` (functional check of the N > 1 logic with every rank on cuda:0;
+    its timings mean nothing): gloo has no device collectives beyond
+    all-reduce / broadcast, so the exchanges stage through host memory."""
 
-    world, rank, local = dist_env()
-    if world > 1:
-        import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    else:
-        torch.cuda.set_device(0)
-    dev = torch.device("cuda", torch.cuda.current_device())
-    c, S, K, h = workload(args.config)
-    params = (S, K, h)
-    n_items = c.get("batch", 1)
-    mode = dist_mode(args.config, world, args.c5_dist)
-    slab, halo, fused = mode == "slab", mode in ("halo", "fused"), mode == "fused"
-    if c["kind"] == "signal" or mode:
-        lo, hi = 0, 1
-    else:  # weak scaling: every rank its own batch of n_items images
-        lo, hi = rank * n_items, (rank + 1) * n_items
-    if slab:
-        from paper_1407_2343_b200.distributed import SlabPlan
-        plan = SlabPlan(c["rows"], c["cols"], world, rank)
-        imgs_host = make_inputs(args.config, 0, 1, row_range=plan.rows)
-    elif halo:
-        from paper_1407_2343_b200.distributed import HaloPlan
-        plan = HaloPlan(c["rows"], c["cols"], world, rank, params)
-        imgs_host = make_inputs(args.config, 0, 1, row_range=plan.rows)
-    else:
-        imgs_host = make_inputs(args.config, lo, hi)
-    x = torch.from_numpy(imgs_host).to(dev)
-    y = torch.empty_like(x)
-    mid = torch.empty_like(x)
-    stream = torch.cuda.current_stream()
-    signal = c["kind"] == "signal"
-    if slab:
-        cb = c["cols"] // world
-        recv = torch.empty_like(x)
-        y = torch.empty((c["rows"], cb), dtype=x.dtype, device=dev)
-    if halo:
-        (olo, ohi), (wlo, whi) = plan.rows, plan.window_rows
-        seg_a, seg_b = plan.segments
-        win = torch.empty((whi - wlo, c["cols"]), dtype=x.dtype, device=dev)
-        y = torch.empty((ohi - olo, c["cols"]), dtype=x.dtype, device=dev)
-        p2p = []
-        if fused:
-            from paper_1407_2343_b200.distributed import symmetric_windows
-            ok = torch.ones(1, device=dev)
-            try:
-                windows, sym_barrier = symmetric_windows(plan, dev)
-                fan = [(windows(d_)[row_:row_ + (hi_ - lo_)], lo_ - olo, hi_ - olo)
-                       for d_, lo_, hi_, row_ in plan.fanout()]
-                if len(fan) > pl.PL_MAX_FANOUT:
-                    raise RuntimeError("more than PL_MAX_FANOUT neighbours")
-            except Exception as e:  # no symmetric memory here: NCCL halo exchange instead
-                print(f"rank {rank}: fused halo unavailable ({e}); using NCCL send/recv",
-                      file=sys.stderr)
-                ok.zero_()
-            torch.distributed.all_reduce(ok, op=torch.distributed.ReduceOp.MIN)
-            if ok.item() > 0:
-                win = windows(rank)[:whi - wlo]
+    def __init__(self, backend: str):
+        import torch
+        self.world, self.rank, self.local = dist_env()
+        self.backend = backend
+        self.d = None
+        if self.world > 1:
+            import torch.distributed as dist
+            self.d = dist
+            if backend == "nccl":
+                torch.cuda.set_device(self.local)
+                dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
             else:
-                fused = False
-        for s_, d_, lo_, hi_ in ([] if fused else plan.transfers()):
-            if s_ == rank:
-                p2p.append(torch.distributed.P2POp(torch.distributed.isend,
-                                                   win[lo_ - wlo:hi_ - wlo], d_))
-            elif d_ == rank:
-                p2p.append(torch.distributed.P2POp(torch.distributed.irecv,
-                                                   win[lo_ - wlo:hi_ - wlo], s_))
+                torch.cuda.set_device(0)
+                dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(0)
+        self.dev = torch.device("cuda", torch.cuda.current_device())
 
-    def first_pass():
-        if signal:
-            pl.nlm_1d_patchlift(x, params, out=y)
-        elif slab:
-            pl.nlm_row_pass_blocked(x, params, cb, out=mid)
-            torch.distributed.all_to_all_single(recv.reshape(-1), mid.reshape(-1))
-        elif fused:
-            sym_barrier()  # peers done reading their windows (previous column pass)
-            pl.nlm_row_pass_fanout(x[0], params, out=win[olo - wlo:ohi - wlo], extras=fan)
-            sym_barrier()  # every halo row delivered
-        elif halo:
-            pl.nlm_row_pass(x[0], params, out=win[olo - wlo:ohi - wlo])
-            if p2p:
-                for req in torch.distributed.batch_isend_irecv(p2p):
-                    req.wait()
-        else:  # row pass into the transposed intermediate (what pl_snlm_2d_row_col runs)
-            R_, C_ = c["rows"], c["cols"]
-            pl.nlm_pass_strided(x, mid, x.shape[0], R_, C_, C_, 1, 1, R_, R_ * C_, params)
+    def _red(self, v: float, op) -> float:
+        import torch
+        if not self.d:
+            return float(v)
+        dev = self.dev if self.backend == "nccl" else "cpu"
+        t = torch.tensor([float(v)], dtype=torch.float64, device=dev)
+        self.d.all_reduce(t, op=op)
+        return float(t.item())
 
-    def second_pass():
-        if signal:
+    def max(self, v: float) -> float:
+        return self._red(v, self.d.ReduceOp.MAX if self.d else None)
+
+    def min(self, v: float) -> float:
+        return self._red(v, self.d.ReduceOp.MIN if self.d else None)
+
+    def barrier(self):
+        if self.d:
+            self.d.barrier()
+
+    def all_to_all(self, recv, send):
+        if self.backend == "nccl":
+            self.d.all_to_all_single(recv, send)
+        else:
+            r = recv.cpu()
+            self.d.all_to_all_single(r, send.cpu())
+            recv.copy_(r)
+
+    def p2p(self, ops):
+        """ops: [("send"|"recv", peer, tensor)], all completed on return."""
+        if not ops:
             return
-        if slab:
-            pl.nlm_col_pass(recv.reshape(c["rows"], cb), params, out=y)
-        elif halo:
-            pl.nlm_col_pass_window(win, wlo, c["rows"], seg_a, seg_b, params, out=y)
-        else:  # column pass reading the transposed intermediate
-            R_, C_ = c["rows"], c["cols"]
-            pl.nlm_pass_strided(mid, y, x.shape[0], C_, R_, R_, 1, 1, C_, R_ * C_, params)
+        if self.backend == "nccl":
+            p2p = [self.d.P2POp(self.d.isend if k == "send" else self.d.irecv, t, peer)
+                   for k, peer, t in ops]
+            for req in self.d.batch_isend_irecv(p2p):
+                req.wait()
+            return
+        reqs, back = [], []
+        for k, peer, t in ops:
+            h = t.cpu() if k == "send" else torch_empty_like_cpu(t)
+            reqs.append((self.d.isend if k == "send" else self.d.irecv)(h, peer))
+            if k == "recv":
+                back.append((t, h))
+        for r in reqs:
+            r.wait()
+        for t, h in back:
+            t.copy_(h)
 
-    def step():
+    def gather_rows(self, full, part):
+        """Rank 0: full = rows of every rank's equal-sized part, in rank order."""
+        if not self.d:
+            full.copy_(part)
+            return
+        if self.backend == "nccl":
+            self.d.all_gather_into_tensor(full, part)
+        else:
+            parts = [torch_empty_like_cpu(part) for _ in range(self.world)]
+            self.d.all_gather(parts, part.cpu())
+            if full is not None:
+                full.copy_(torch_cat(parts))
+
+    def broadcast(self, t, src=0):
+        if not self.d:
+            return
+        if self.backend == "nccl":
+            self.d.broadcast(t, src)
+        else:
+            h = t.cpu()
+            self.d.broadcast(h, src)
+            t.copy_(h)
+
+    def close(self):
+        if self.d:
+            self.d.barrier()
+            self.d.destroy_process_group()
+
+
+def torch_empty_like_cpu(t):
+    import torch
+    return torch.empty(tuple(t.shape), dtype=t.dtype)
+
+
+def torch_cat(parts):
+    import torch
+    return torch.cat(parts, 0)
+
+
+def timed(D, first_pass, second_pass, steps, warmup, clocks=True):
+    """W warm-up steps, then K steps between two events on the launching
+    stream (per-pass events inside), barrier + synchronize on both sides;
+    the step time is the max over ranks."""
+    import torch
+    stream = torch.cuda.current_stream()
+    for _ in range(max(3, warmup)):
         first_pass()
         second_pass()
-
-    for _ in range(max(3, args.warmup)):
-        step()
     torch.cuda.synchronize()
-
-    # per-launch timing of the two pass kernels (events on the launching stream)
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(steps)]
     start = torch.cuda.Event(enable_timing=True)
     end = torch.cuda.Event(enable_timing=True)
-    if world > 1:
-        torch.distributed.barrier()
+    D.barrier()
     torch.cuda.synchronize()
-    with ClockSampler(dev.index) as clocks:
+    sampler = ClockSampler(D.dev.index) if clocks else None
+    if sampler:
+        sampler.__enter__()
+    try:
         start.record(stream)
-        for k in range(args.steps):
+        for k in range(steps):
             ev[k][0].record(stream)
             first_pass()
             ev[k][1].record(stream)
@@ -396,175 +419,449 @@ def run_ours(args):
             ev[k][2].record(stream)
         end.record(stream)
         torch.cuda.synchronize()
-        # keep sampling a short moment so very short regions still get clock samples
-        if len(clocks.lines) < 3:
-            time.sleep(0.35)
-    if world > 1:
-        torch.distributed.barrier()
-    ms_local = start.elapsed_time(end)
-    t = torch.tensor([ms_local], device=dev, dtype=torch.float64)
-    if world > 1:
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-    ms_total = float(t.item())
-    ms_step = ms_total / args.steps
-    row_ms = [ev[k][0].elapsed_time(ev[k][1]) for k in range(args.steps)]
-    col_ms = [ev[k][1].elapsed_time(ev[k][2]) for k in range(args.steps)]
+        if sampler and len(sampler.lines) < 3:
+            time.sleep(0.35)  # very short regions still get clock samples
+    finally:
+        if sampler:
+            sampler.__exit__(None, None, None)
+    D.barrier()
+    ms_step = D.max(start.elapsed_time(end)) / steps
+    return {"ms_step": ms_step,
+            "row_ms": float(np.mean([e[0].elapsed_time(e[1]) for e in ev])),
+            "col_ms": float(np.mean([e[1].elapsed_time(e[2]) for e in ev])),
+            "clocks": sampler.summary() if sampler else None}
 
-    if signal:
-        px_local = c["n"]
-        px_total = px_local
-    elif mode:
-        px_local = x.numel() if halo else c["rows"] * c["cols"] // world
-        px_total = c["rows"] * c["cols"]
-    else:
-        px_local = (hi - lo) * c["rows"] * c["cols"]
-        px_total = world * n_items * c["rows"] * c["cols"]
-    value = px_total / (ms_step * 1e-3) / 1e6
 
-    # ---- roofline (dominant kernel): unique pairs = exps per launch ----------
-    if signal:
-        u_row = pl.unique_pairs(c["n"], S)
-        u_col = 0
-    elif slab:
-        u_row = (c["rows"] // world) * pl.unique_pairs(c["cols"], S)
-        u_col = (c["cols"] // world) * pl.unique_pairs(c["rows"], S)
-    elif halo:  # pairs counted at their left endpoint, which my rows own
-        u_row = (ohi - olo) * pl.unique_pairs(c["cols"], S)
-        u_col = c["cols"] * sum(min(S, c["rows"] - 1 - i) for i in range(olo, ohi))
-    else:
-        u_row = (hi - lo) * c["rows"] * pl.unique_pairs(c["cols"], S)
-        u_col = (hi - lo) * c["cols"] * pl.unique_pairs(c["rows"], S)
-    row_avg = float(np.mean(row_ms))
-    col_avg = float(np.mean(col_ms)) if not signal else 0.0
-    dom = "row" if row_avg * 1.0 >= col_avg else "col"
+def roofline(D, u_row, u_col, t, px_local, cfg_name, sms, f_max, live_peaks):
+    """Roofline of SURVEY.md sec. 8(d) for the dominant pass kernel: per unique
+    pair 1 MUFU.EX2 + 8 FP32 lane-ops, per pass 8 HBM bytes per pixel.
+    ``frac`` is against the NOMINAL peak (16 EX2 = 128/8 FP32 lanes per clock
+    per SM at the maximum SM clock); the live-measured
+    MUFU / FP32 peaks of this GPU are a secondary denominator."""
+    row_avg, col_avg = t["row_ms"], t["col_ms"]
+    dom = "row" if row_avg >= col_avg else "col"
     u_dom, t_dom = (u_row, row_avg) if dom == "row" else (u_col, col_avg)
-    peaks = measured_peaks()
-    ex2_peak, ffma_peak = (mufu_peak() if rank == 0 else (None, None))
-    f_max = peaks.get("sm_max_mhz", 1965.0) * 1e6
-    sms = torch.cuda.get_device_properties(dev).multi_processor_count
-    # Roofline of SURVEY.md sec. 8(d): per unique pair 1 MUFU.EX2 + 8 FP32 lane-ops,
-    # per pass 8 HBM bytes per pixel.  Peaks measured live on this GPU
-    # (lib/libplubench.so); nominal: 16 ex2 and 128 FP32 lanes per clock per SM.
-    ex2_rate = ex2_peak or 16 * sms * f_max
-    fp32_rate = ffma_peak or 128 * sms * f_max
-    pair_peak = min(ex2_rate, fp32_rate / 8.0)  # pairs/s
+    nominal = 16 * sms * f_max  # pairs/s
+    ex2_peak, ffma_peak = live_peaks
+    live = min(ex2_peak or nominal, (ffma_peak or 8 * nominal) / 8.0)
     achieved = u_dom / (t_dom * 1e-3)
-    hbm_bytes = 8 * px_local  # per pass: fp32 read + write
-    hbm_gbs = peaks.get("hbm_gbs", 6541.5)
-    roof = {
-        "bound": "fp32" if fp32_rate / 8.0 < ex2_rate else "sfu",
-        "achieved": achieved / 1e9, "peak": pair_peak / 1e9, "unit": "Gpair/s",
-        "frac": achieved / pair_peak, "traffic": ncu_traffic(args.config),
+    hbm_bytes = 8 * px_local
+    hbm_gbs = measured_peaks().get("hbm_gbs", 6541.5)
+    return {
+        "bound": "sfu+fp32 (tie: 1 EX2 and 8 FP32 lane-ops per pair)",
+        "achieved": achieved / 1e9, "peak": nominal / 1e9, "unit": "Gpair/s",
+        "frac": achieved / nominal, "traffic": ncu_traffic(cfg_name),
+        "peak_kind": "nominal: 16 MUFU.EX2 (= 128 FP32 lanes / 8 ops) per clock per SM "
+                     f"x {sms} SMs x {f_max / 1e6:.0f} MHz",
         "kernel": f"nlm_pass3_kernel ({dom} pass)",
-        "definition": "unique in-band pairs U per launch / CUDA-event launch time; peak = "
-                      "min(MUFU.EX2 rate, FP32 lane-op rate / 8), both measured live",
-        "ex2_peak_gexp_s": ex2_rate / 1e9, "fp32_peak_glaneops_s": fp32_rate / 1e9,
-        "frac_of_ex2": achieved / ex2_rate,
-        "peak_nominal_gpair_s": 16 * sms * f_max / 1e9,
+        "definition": "unique in-band pairs U per launch / CUDA-event launch time",
+        "frac_measured_peak": achieved / live, "measured_peak_gpair_s": live / 1e9,
+        "ex2_peak_gexp_s": (ex2_peak or 0) / 1e9, "fp32_peak_glaneops_s": (ffma_peak or 0) / 1e9,
         "algorithmic_per_launch": {"pairs": u_dom, "exps": u_dom, "fp32_ops": 8 * u_dom,
                                    "hbm_bytes": hbm_bytes},
         "row_pass_ms": row_avg, "col_pass_ms": col_avg,
-        "step_frac": (u_row + u_col) / (ms_step * 1e-3) / pair_peak,
+        "step_frac": (u_row + u_col) / (t["ms_step"] * 1e-3) / nominal,
         "hbm": {"achieved_gbs": hbm_bytes / (t_dom * 1e-3) / 1e9, "peak_gbs": hbm_gbs,
                 "t_hbm_ms": hbm_bytes / (hbm_gbs * 1e9) * 1e3},
     }
 
-    line = None
+
+class BatchRun:
+    """Independent images (c2-c4) or the c1 signal: images [lo, hi) of the
+    workload on this rank, no communication.  One step = the row pass into
+    the transposed intermediate + the column pass (what pl_snlm_2d_row_col
+    runs)."""
+
+    def __init__(self, D, pl, cfg_name, lo, hi, params):
+        import torch
+        self.pl, self.params, self.cfg_name = pl, params, cfg_name
+        c = W_CONFIGS()[cfg_name]
+        self.c = c
+        self.signal = c["kind"] == "signal"
+        self.imgs_host = make_inputs(cfg_name, lo, hi)
+        self.n_local = hi - lo
+        self.x = torch.from_numpy(self.imgs_host).to(D.dev)
+        self.y = torch.empty_like(self.x)
+        self.mid = torch.empty_like(self.x)
+        S = params[0]
+        if self.signal:
+            self.px_local = c["n"]
+            self.u_row, self.u_col = pl.unique_pairs(c["n"], S), 0
+        else:
+            self.px_local = self.n_local * c["rows"] * c["cols"]
+            self.u_row = self.n_local * c["rows"] * pl.unique_pairs(c["cols"], S)
+            self.u_col = self.n_local * c["cols"] * pl.unique_pairs(c["rows"], S)
+
+    def first_pass(self):
+        if self.signal:
+            self.pl.nlm_1d_patchlift(self.x, self.params, out=self.y)
+            return
+        R_, C_ = self.c["rows"], self.c["cols"]
+        if self.n_local:
+            self.pl.nlm_pass_strided(self.x, self.mid, self.n_local, R_, C_, C_, 1, 1, R_, R_ * C_,
+                                     self.params)
+
+    def second_pass(self):
+        if self.signal or not self.n_local:
+            return
+        R_, C_ = self.c["rows"], self.c["cols"]
+        self.pl.nlm_pass_strided(self.mid, self.y, self.n_local, C_, R_, R_, 1, 1, C_, R_ * C_,
+                                 self.params)
+
+    def e2e(self, D, steps):
+        """Through the C-ABI host entry point (pinned host buffers, H2D + D2H
+        inside); max over ranks.  Returns (seconds per step, bytes in, out, ok)."""
+        import torch
+        hin = torch.from_numpy(self.imgs_host).pin_memory()
+        if self.signal:
+            t0 = time.perf_counter()
+            for _ in range(steps):
+                yh = self.pl.nlm_1d_patchlift(hin.to(D.dev, non_blocking=True), self.params).cpu()
+            return (time.perf_counter() - t0) / steps, hin.numel() * 4, yh.numel() * 4, None
+        hout = torch.empty_like(hin).pin_memory()
+        if self.n_local:
+            self.pl.snlm_2d_row_col_host(hin, self.params, hout)  # warm-up
+        D.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            if self.n_local:
+                self.pl.snlm_2d_row_col_host(hin, self.params, hout)
+        e2e_s = D.max((time.perf_counter() - t0) / steps)
+        ok = bool(torch.equal(hout, self.y.cpu()))
+        return e2e_s, hin.numel() * 4, hout.numel() * 4, D.min(1.0 if ok else 0.0) > 0
+
+
+def W_CONFIGS():
+    from paper_1407_2343_b200 import workloads as W
+    return W.CONFIGS
+
+
+class C5Run:
+    """One 16384^2 image over G ranks (north_star config c5), three forms:
+    ``slab`` (row slabs -> row pass into the all-to-all send layout -> NCCL
+    all-to-all -> column pass on the column slab, the north-star design),
+    ``halo`` (row partition by whole column segments + NCCL halo send/recv +
+    windowed column pass) and ``fused`` (the same partition, halo rows stored
+    into the neighbours' symmetric-memory windows by the row-pass kernel)."""
+
+    def __init__(self, D, pl, form, params, cfg_name="c5"):
+        import torch
+        self.D, self.pl, self.form, self.params = D, pl, form, params
+        c = W_CONFIGS()[cfg_name]
+        self.c = c
+        H, Wd = c["rows"], c["cols"]
+        world, rank = D.world, D.rank
+        S = params[0]
+        dev = D.dev
+        if form == "slab":
+            from paper_1407_2343_b200.distributed import SlabPlan
+            self.plan = plan = SlabPlan(H, Wd, world, rank)
+            self.imgs_host = make_inputs(cfg_name, 0, 1, row_range=plan.rows)
+            self.cb = Wd // world
+            self.x = torch.from_numpy(self.imgs_host).to(dev)
+            self.mid = torch.empty_like(self.x)
+            self.recv = torch.empty_like(self.x)
+            self.y = torch.empty((H, self.cb), dtype=torch.float32, device=dev)
+            self.region = ("cols",) + plan.cols
+            self.nvlink_bytes = plan.nvlink_bytes()
+            self.parallelism = f"row slabs -> NCCL all-to-all -> column slabs x{world}"
+            self.u_row = (H // world) * pl.unique_pairs(Wd, S)
+            self.u_col = self.cb * pl.unique_pairs(H, S)
+            self.px_local = H * Wd // world
+            return
+        from paper_1407_2343_b200.distributed import HaloPlan
+        self.plan = plan = HaloPlan(H, Wd, world, rank, params)
+        (olo, ohi), (wlo, whi) = plan.rows, plan.window_rows
+        self.olo, self.ohi, self.wlo, self.whi = olo, ohi, wlo, whi
+        self.seg = plan.segments
+        self.imgs_host = make_inputs(cfg_name, 0, 1, row_range=plan.rows)
+        self.x = torch.from_numpy(self.imgs_host).to(dev)
+        self.y = torch.empty((ohi - olo, Wd), dtype=torch.float32, device=dev)
+        self.region = ("rows", olo, ohi)
+        self.nvlink_bytes = plan.halo_bytes()
+        self.u_row = (ohi - olo) * pl.unique_pairs(Wd, S)
+        self.u_col = Wd * sum(min(S, H - 1 - i) for i in range(olo, ohi))
+        self.px_local = (ohi - olo) * Wd
+        if form == "fused":
+            self._setup_fused()
+            self.parallelism = f"row partition (whole column segments) + fused NVLink halo stores x{world}"
+        else:
+            self.win = torch.empty((whi - wlo, Wd), dtype=torch.float32, device=dev)
+            self.parallelism = f"row partition (whole column segments) + NCCL halo send/recv x{world}"
+        self.ops = []
+        if form == "halo":
+            for s_, d_, lo_, hi_ in plan.transfers():
+                if s_ == rank:
+                    self.ops.append(("send", d_, self.win[lo_ - wlo:hi_ - wlo]))
+                elif d_ == rank:
+                    self.ops.append(("recv", s_, self.win[lo_ - wlo:hi_ - wlo]))
+
+    def _setup_fused(self):
+        """Symmetric-memory windows, probed without any collective first so a
+        rank that cannot allocate them never leaves its peers in a rendezvous
+        (every rank agrees, then all rendezvous or none does)."""
+        import torch
+        D, plan = self.D, self.plan
+        ok = 1.0
+        if D.backend != "nccl":
+            ok = 0.0
+        else:
+            try:
+                import torch.distributed._symmetric_memory as symm
+                symm.empty(1, dtype=torch.float32, device=D.dev)
+            except Exception as e:  # noqa: BLE001 -- reported, then every rank agrees
+                print(f"rank {D.rank}: symmetric memory unavailable ({e})", file=sys.stderr)
+                ok = 0.0
+        if D.min(ok) <= 0:
+            raise RuntimeError("symmetric memory unavailable on some rank")
+        from paper_1407_2343_b200.distributed import symmetric_windows
+        self.windows, self.sym_barrier = symmetric_windows(plan, D.dev)
+        self.fan = [(self.windows(d_)[row_:row_ + (hi_ - lo_)], lo_ - self.olo, hi_ - self.olo)
+                    for d_, lo_, hi_, row_ in plan.fanout()]
+        if len(self.fan) > self.pl.PL_MAX_FANOUT:
+            raise RuntimeError("more than PL_MAX_FANOUT neighbours")
+        self.win = self.windows(D.rank)[:self.whi - self.wlo]
+
+    def first_pass(self):
+        pl, p = self.pl, self.params
+        if self.form == "slab":
+            pl.nlm_row_pass_blocked(self.x, p, self.cb, out=self.mid)
+            self.D.all_to_all(self.recv.reshape(-1), self.mid.reshape(-1))
+        elif self.form == "fused":
+            self.sym_barrier()  # peers done reading their windows (previous column pass)
+            pl.nlm_row_pass_fanout(self.x[0], p, out=self.win[self.olo - self.wlo:self.ohi - self.wlo],
+                                   extras=self.fan)
+            self.sym_barrier()  # every halo row delivered
+        else:
+            pl.nlm_row_pass(self.x[0], p, out=self.win[self.olo - self.wlo:self.ohi - self.wlo])
+            self.D.p2p(self.ops)
+
+    def second_pass(self):
+        pl, p = self.pl, self.params
+        if self.form == "slab":
+            pl.nlm_col_pass(self.recv.reshape(self.c["rows"], self.cb), p, out=self.y)
+        else:
+            pl.nlm_col_pass_window(self.win, self.wlo, self.c["rows"], self.seg[0], self.seg[1], p,
+                                   out=self.y)
+
+    def matches(self, ref):
+        """Bitwise equal to the single-GPU RC (ref: the whole image)."""
+        import torch
+        kind, a, b = self.region
+        want = ref[:, a:b] if kind == "cols" else ref[a:b]
+        ok = bool(torch.equal(self.y, want))
+        return self.D.min(1.0 if ok else 0.0) > 0
+
+    def e2e(self, steps):
+        import torch
+        hin = torch.from_numpy(self.imgs_host).pin_memory()
+        hout = torch.empty(tuple(self.y.shape), dtype=torch.float32).pin_memory()
+        torch.cuda.synchronize()
+        self.D.barrier()
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            self.x.copy_(hin, non_blocking=True)
+            self.first_pass()
+            self.second_pass()
+            hout.copy_(self.y, non_blocking=True)
+            torch.cuda.synchronize()
+        return (self.D.max((time.perf_counter() - t0) / steps), hin.numel() * 4 * self.D.world,
+                hout.numel() * 4 * self.D.world)
+
+
+def c5_reference(D, pl, params, slab_input):
+    """Single-GPU RC of the whole c5 image on rank 0 (its rows gathered from
+    the slab form's row slabs), broadcast to every rank for the bitwise check."""
+    import torch
+    c = W_CONFIGS()["c5"]
+    full = torch.empty((c["rows"], c["cols"]), dtype=torch.float32, device=D.dev)
+    D.gather_rows(full, slab_input.reshape(-1, c["cols"]))
+    if D.rank == 0:
+        ref = pl.snlm_2d_row_col(full, params)
+    else:
+        ref = torch.empty_like(full)
+    del full
+    D.broadcast(ref, 0)
+    return ref
+
+
+def c5_forms(D, pl, params, args, forms):
+    """Time each c5 form (device, max over ranks) and check it bitwise against
+    the single-GPU RC.  Returns {form: {...}} (unavailable forms say why)."""
+    import torch
+    out = {}
+    ref = None
+    for form in forms:
+        try:
+            run = C5Run(D, pl, form, params)
+        except RuntimeError as e:
+            out[form] = {"unavailable": str(e)}
+            continue
+        t = timed(D, run.first_pass, run.second_pass, args.steps, args.warmup, clocks=False)
+        if ref is None:
+            slab = run.x if form == "slab" else None
+            if slab is None:
+                from paper_1407_2343_b200.distributed import SlabPlan
+                sp = SlabPlan(run.c["rows"], run.c["cols"], D.world, D.rank)
+                slab = torch.from_numpy(make_inputs("c5", 0, 1, row_range=sp.rows)).to(D.dev)
+            ref = c5_reference(D, pl, params, slab)
+        px = run.c["rows"] * run.c["cols"]
+        out[form] = {"value": px / (t["ms_step"] * 1e-3) / 1e6, "unit": UNIT,
+                     "ms_per_step": t["ms_step"], "row_pass_ms": t["row_ms"],
+                     "col_pass_ms": t["col_ms"], "nvlink_bytes_per_rank": run.nvlink_bytes,
+                     "parallelism": run.parallelism,
+                     "bitwise_equal_single_gpu_rc": run.matches(ref)}
+        del run
+        torch.cuda.empty_cache()
+    return out
+
+
+def run_ours(args):
+    import torch
+    import paper_1407_2343_b200 as pl
+
+    D = Dist(args.dist_backend)
+    world, rank = D.world, D.rank
+    c, S, K, h = workload(args.config)
+    params = (S, K, h)
+    n_items = c.get("batch", 1)
+    f_max = measured_peaks().get("sm_max_mhz", 1965.0) * 1e6
+    sms = torch.cuda.get_device_properties(D.dev).multi_processor_count
+    live_peaks = mufu_peak() if rank == 0 else (None, None)
+    cfg = arm_config(args.config, world)
+    c5_main = args.config == "c5" and world > 1
+
+    if c5_main:
+        # the chosen form is the line; the other two ride along as fields
+        run = C5Run(D, pl, args.c5_dist, params)
+        t = timed(D, run.first_pass, run.second_pass, args.steps, args.warmup)
+        px_total = c["rows"] * c["cols"]
+        roof = roofline(D, run.u_row, run.u_col, t, run.px_local, args.config, sms, f_max, live_peaks)
+        e2e_s, bi, bo = run.e2e(args.e2e_steps)
+        e2e = {"value": px_total / e2e_s / 1e6, "unit": UNIT, "h2d_bytes_per_step": bi,
+               "d2h_bytes_per_step": bo,
+               "api": f"pinned H2D + c5 {args.c5_dist} path (row pass, exchange, column pass) + D2H"}
+        cfg["parallelism"] = run.parallelism
+        cfg["nvlink_bytes_per_rank"] = run.nvlink_bytes
+        launches = args.steps * 2
+        del run
+        torch.cuda.empty_cache()
+        extra = {"c5_forms": c5_forms(D, pl, params, args, ["slab", "halo", "fused"])}
+        scaling = "strong"
+    else:
+        if c["kind"] == "signal":
+            lo, hi = 0, 1
+        else:  # BASELINE's batch sharded across the ranks (contiguous shares)
+            from paper_1407_2343_b200.distributed import shard
+            lo, hi = shard(n_items, world, rank)
+        run = BatchRun(D, pl, args.config, lo, hi, params)
+        t = timed(D, run.first_pass, run.second_pass, args.steps, args.warmup)
+        px_total = c["n"] if run.signal else n_items * c["rows"] * c["cols"]
+        roof = roofline(D, run.u_row, run.u_col, t, run.px_local, args.config, sms, f_max, live_peaks)
+        e2e_s, bi, bo, ok = run.e2e(D, args.e2e_steps)
+        e2e = {"value": px_total / e2e_s / 1e6, "unit": UNIT,
+               "h2d_bytes_per_step": int(D.max(bi) * world) if world > 1 else bi,
+               "d2h_bytes_per_step": int(D.max(bo) * world) if world > 1 else bo}
+        if not run.signal:
+            e2e["api"] = "pl_snlm_2d_row_col_host (pinned host buffers)"
+            e2e["matches_device_result"] = ok
+        launches = args.steps * (1 if run.signal else 2)
+        scaling = "strong"
+        extra = {}
+        if world > 1 and not run.signal:
+            # weak form: every rank its own full batch (images 64r .. 64r+63)
+            del run
+            torch.cuda.empty_cache()
+            wk = BatchRun(D, pl, args.config, rank * n_items, (rank + 1) * n_items, params)
+            tw = timed(D, wk.first_pass, wk.second_pass, args.steps, args.warmup, clocks=False)
+            extra["weak"] = {"value": world * n_items * c["rows"] * c["cols"] / (tw["ms_step"] * 1e-3) / 1e6,
+                             "unit": UNIT, "ms_per_step": tw["ms_step"], "images_per_rank": n_items,
+                             "scaling": "weak"}
+            del wk
+            torch.cuda.empty_cache()
+        if world > 1 and args.config == "c4" and not args.no_c5_forms:
+            # the north-star single-image path rides along at N > 1 (all three forms)
+            extra["c5_forms"] = c5_forms(D, pl, workload("c5")[1:], args,
+                                         ["slab", "halo", "fused"])
+
+    value = px_total / (t["ms_step"] * 1e-3) / 1e6
     if rank == 0:
-        cfg = describe(args.config, c, S, K, h, n_items)
-        cfg["l2"] = ("inputs + intermediate exceed the 126 MB L2" if px_total * 4 > 126e6
-                     else "working set fits L2 (flush not applied; compute-bound kernel)")
-        cfg["parallelism"] = (f"{world} ranks x {n_items} images each (no communication)"
-                              if world > 1 else "1 GPU")
-        if not (mode or signal):
-            cfg["global_batch"] = world * n_items
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "strong" if (mode or signal) else "weak", "vs_baseline": None,
-            "dtype": "f32",
+            "warmup": max(3, args.warmup), "ms_per_step": t["ms_step"], "higher_is_better": True,
+            "scaling": scaling, "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded PCG64 constructions of BASELINE.json, "
                     "paper_1407_2343_b200/workloads.py)",
-            "config": cfg, "roofline": roof, "clocks": clocks.summary(),
-            "gpu_launches": args.steps * (1 if signal else 2),
+            "config": cfg, "roofline": roof, "clocks": t["clocks"], "gpu_launches": launches,
+            "e2e": e2e,
         }
-
-    # ---- e2e through the C-ABI host entry point (N GPUs: each rank its shard) --
-    if mode:
-        hin = torch.from_numpy(imgs_host).pin_memory()
-        hout = torch.empty(tuple(y.shape), dtype=torch.float32).pin_memory()
-        torch.cuda.synchronize()
-        torch.distributed.barrier()
-        t0 = time.perf_counter()
-        for _ in range(args.e2e_steps):
-            x.copy_(hin, non_blocking=True)
-            step()
-            hout.copy_(y, non_blocking=True)
-            torch.cuda.synchronize()
-        e2e_s = (time.perf_counter() - t0) / args.e2e_steps
-        te = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
-        torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
-        if rank == 0:
-            line["e2e"] = {"value": px_total / float(te.item()) / 1e6, "unit": UNIT,
-                           "h2d_bytes_per_step": int(hin.numel() * 4) * world,
-                           "d2h_bytes_per_step": int(hout.numel() * 4) * world}
-            if slab:
-                line["e2e"]["api"] = "pinned H2D + row pass + NCCL all-to-all + column pass + D2H"
-                line["config"]["nvlink_bytes_per_rank"] = plan.nvlink_bytes()
-                line["config"]["parallelism"] = f"row slabs -> all-to-all -> column slabs x{world}"
-            else:
-                line["e2e"]["api"] = ("pinned H2D + row pass + " +
-                                      ("fused NVLink halo stores (symmetric memory) + barrier"
-                                       if fused else "NCCL halo send/recv") +
-                                      " + windowed column pass + D2H")
-                line["config"]["nvlink_bytes_per_rank"] = plan.halo_bytes()
-                line["config"]["parallelism"] = (f"row partition (whole column segments) + "
-                                                 f"{'fused NVLink halo stores' if fused else 'halo exchange'} x{world}")
-    elif not signal:
-        hin = torch.from_numpy(imgs_host).pin_memory()
-        hout = torch.empty_like(hin).pin_memory()
-        pl.snlm_2d_row_col_host(hin, params, hout)  # warm-up
-        if world > 1:
-            torch.distributed.barrier()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        for _ in range(args.e2e_steps):
-            pl.snlm_2d_row_col_host(hin, params, hout)
-        e2e_s = (time.perf_counter() - t0) / args.e2e_steps
-        te = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
-        if world > 1:
-            torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
-        e2e_s = float(te.item())
-        ok = torch.equal(hout, y.cpu())
-        if rank == 0:
-            line["e2e"] = {"value": px_total / e2e_s / 1e6, "unit": UNIT,
-                           "h2d_bytes_per_step": int(hin.numel() * 4) * world,
-                           "d2h_bytes_per_step": int(hout.numel() * 4) * world,
-                           "api": "pl_snlm_2d_row_col_host (pinned host buffers)",
-                           "matches_device_result": bool(ok)}
-    elif rank == 0:
-        hin = torch.from_numpy(imgs_host).pin_memory()
-        t0 = time.perf_counter()
-        for _ in range(args.e2e_steps):
-            xd = hin.to(dev, non_blocking=True)
-            yd = pl.nlm_1d_patchlift(xd, params)
-            yh = yd.cpu()
-        e2e_s = (time.perf_counter() - t0) / args.e2e_steps
-        line["e2e"] = {"value": px_total / e2e_s / 1e6, "unit": UNIT,
-                       "h2d_bytes_per_step": int(hin.numel() * 4),
-                       "d2h_bytes_per_step": int(yh.numel() * 4)}
-
-    # ---- CPU baseline (rank 0, N=1 only) ----------------------------------------
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, cores, sample, kind = cpu_reference_rate(args.config, imgs_host, S, K, h,
-                                                    args.cpu_seconds)
-        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": kind,
-                                "sample": sample}
-    if rank == 0:
+        if D.backend != "nccl":
+            line["functional_check_only"] = "gloo backend, all ranks on cuda:0: timings meaningless"
+        line.update(extra)
+        if world == 1 and not c5_main and not run.signal:
+            line["e2e_dropin"] = dropin_e2e(run.imgs_host[0], S, K, h, args.e2e_steps)
+        if world == 1 and not args.no_cpu_baseline:
+            v, cores, sample, kind = cpu_reference_rate(args.config, run.imgs_host, S, K, h,
+                                                        args.cpu_seconds)
+            line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": kind,
+                                    "sample": sample, "cpu_model": cpu_model()}
         print(json.dumps(line), flush=True)
-    if world > 1:
-        torch.distributed.barrier()
-        torch.distributed.destroy_process_group()
+    D.close()
+
+
+def dropin_e2e(img, S, K, h, calls):
+    """Mpixel/s through the C++ drop-in a reference caller links
+    (patchlift::snlm_2d_row_col on a double Image2D, threads=0: conversions,
+    copies and both passes per call), one image of the workload per call."""
+    import tempfile
+    exe = os.path.join(ROOT, "paper_1407_2343_b200", "lib", "dropin_bench")
+    if not os.path.exists(exe):
+        return {"unavailable": "lib/dropin_bench not built"}
+    with tempfile.NamedTemporaryFile(suffix=".f32") as f:
+        np.ascontiguousarray(img, dtype=np.float32).tofile(f.name)
+        r = subprocess.run([exe, f.name, str(img.shape[0]), str(img.shape[1]), str(S), str(K),
+                            repr(float(h)), str(max(1, calls)), "0"],
+                           capture_output=True, text=True, timeout=600)
+    if r.returncode != 0:
+        return {"unavailable": (r.stderr or r.stdout).strip()[-300:]}
+    out = json.loads(r.stdout.strip().splitlines()[-1])
+    return {"value": out["mpx_s"], "unit": UNIT, "s_per_call": out["s_per_call"],
+            "calls": out["calls"], "images_per_call": 1,
+            "api": "patchlift::snlm_2d_row_col (C++ drop-in, double Image2D in and out, "
+                   "threads=0; tests/cpp/dropin_bench.cpp)"}
+
+
+def arm_config(cfg_name, world):
+    """The `config` object both arms print (identical, so the driver compares
+    like with like)."""
+    c, S, K, h = workload(cfg_name)
+    n_items = c.get("batch", 1)
+    cfg = describe(cfg_name, c, S, K, h, n_items)
+    if c["kind"] == "image":
+        px_total = n_items * c["rows"] * c["cols"]
+        cfg["l2"] = ("inputs + intermediate exceed the 126 MB L2" if px_total * 4 > 126e6
+                     else "working set fits L2 (flush not applied; compute-bound kernel)")
+        cfg["global_batch"] = n_items
+    cfg["parallelism"] = ("1 GPU" if world == 1 else
+                          f"{n_items} images sharded over {world} ranks (contiguous, no communication)"
+                          if c["kind"] == "image" and n_items > 1 else f"{world} ranks")
+    return cfg
+
+
+def cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        info = {}
+        for ln in out.splitlines():
+            if ":" in ln:
+                k, v = ln.split(":", 1)
+                info[k.strip()] = v.strip()
+        return {"model": info.get("Model name"), "cpus": info.get("CPU(s)"),
+                "sockets": info.get("Socket(s)"), "cores_per_socket": info.get("Core(s) per socket"),
+                "threads_per_core": info.get("Thread(s) per core")}
+    except (OSError, subprocess.SubprocessError):
+        return None
 
 
 def main():

@@ -201,6 +201,16 @@ int pl_device_free(void* ptr);
 int pl_copy_to_device(void* dst, const void* src, size_t bytes);
 int pl_copy_to_host(void* dst, const void* src, size_t bytes);
 int pl_synchronize(void);
+/* Pinned (page-locked) host staging memory, streams and stream-ordered
+ * copies: what a host layer needs to keep a call's H2D, kernels and D2H on
+ * one stream (the C++ drop-in's per-thread staging context). */
+int pl_host_alloc(void** ptr, size_t bytes);
+int pl_host_free(void* ptr);
+int pl_stream_create(void** stream);
+int pl_stream_destroy(void* stream);
+int pl_stream_synchronize(void* stream);
+int pl_copy_to_device_async(void* dst, const void* src, size_t bytes, void* stream);
+int pl_copy_to_host_async(void* dst, const void* src, size_t bytes, void* stream);
 
 /* ---- distance / kernel bands (BandedKernel layout, banded_kernel.hpp:11-38)
  * band[l][i][o] for pair (i, i+o-S), o in [0, 2S+1); cells whose partner is

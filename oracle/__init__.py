@@ -50,7 +50,7 @@ def build(with_reference: bool | None = None) -> None:
     if with_reference is None:
         with_reference = os.path.isdir(REF_SRC)
     if with_reference:
-        targets.append("ref")
+        targets += ["ref", "acceptance"]
     subprocess.run(["make", "-s", "-C", HERE] + targets, check=True)
 
 

@@ -37,7 +37,9 @@ EXPORTS = [
     "pl_synchronize", "pl_distance_band_f32", "pl_distance_band_i32", "pl_banded_kernel_f64",
     "pl_col_window", "pl_nlm_col_pass_window", "pl_image_metrics_f32", "pl_image_metrics_f64",
     "pl_nlm_pass_strided", "pl_nlm_row_pass_fanout", "pl_last_route",
-    "pl_debug_hot_distance_band",
+    "pl_debug_hot_distance_band", "pl_host_alloc", "pl_host_free", "pl_stream_create",
+    "pl_stream_destroy", "pl_stream_synchronize", "pl_copy_to_device_async",
+    "pl_copy_to_host_async",
 ]
 PL_MAX_FANOUT = 2
 

@@ -12,8 +12,11 @@
 //    search radius is 0 the filter is the identity and the input is returned
 //    bit for bit (nlm_test.cpp:87-99).
 //  * OpCounter receives the reference's closed forms (pl_op_counts_1d).
-//  * `threads` is accepted and ignored: results are invariant to it upstream
-//    too (nlm.cpp:13-17).
+//  * Data movement: a per-thread staging context (stream, pinned host and
+//    device buffers kept between calls); `threads` (0 = all hardware
+//    threads, nlm.cpp:18-54) parallelises the host-side double <-> fp32
+//    conversions.  Results do not depend on it, as upstream (nlm.cpp:13-17).
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <limits>
@@ -22,6 +25,7 @@
 #include <random>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "patchlift/banded_kernel.hpp"
@@ -45,7 +49,7 @@ void check(int rc) {
   if (rc != PL_OK) raise(rc);
 }
 
-// Owning device buffer.
+// Owning device buffer (one-off transfers: F-bar bands, metrics).
 template <typename T>
 class DeviceBuffer {
  public:
@@ -66,15 +70,117 @@ class DeviceBuffer {
   std::size_t count_ = 0;
 };
 
-std::vector<float> to_f32(const std::vector<double>& v) {
-  std::vector<float> out(v.size());
-  for (std::size_t k = 0; k < v.size(); ++k) out[k] = static_cast<float>(v[k]);
-  return out;
+// Host-side conversion work split over `threads` std::threads (the
+// reference's `threads` argument: 0 = hardware_concurrency, nlm.cpp:18-54);
+// small inputs stay on the calling thread; at most 64 workers.
+template <typename F>
+void parallel_chunks(std::size_t count, int threads, F&& fn) {
+  constexpr std::size_t kMinPerThread = std::size_t(1) << 18;
+  unsigned t = threads > 0 ? static_cast<unsigned>(threads) : std::thread::hardware_concurrency();
+  t = std::max(1u, std::min<unsigned>({t, 64u, static_cast<unsigned>(count / kMinPerThread)}));
+  if (t <= 1) {
+    fn(std::size_t(0), count, 0u);
+    return;
+  }
+  std::vector<std::thread> pool;
+  for (unsigned k = 0; k < t; ++k)
+    pool.emplace_back([&, k] { fn(count * k / t, count * (k + 1) / t, k); });
+  for (auto& th : pool) th.join();
 }
 
-std::vector<double> to_f64(const std::vector<float>& v) {
-  std::vector<double> out(v.size());
-  for (std::size_t k = 0; k < v.size(); ++k) out[k] = static_cast<double>(v[k]);
+// Per-thread staging context: one non-blocking stream, device buffers and
+// pinned host buffers that grow and are kept for the thread's later calls,
+// so a call costs the conversions, two stream-ordered copies and the
+// kernels (no cudaMalloc / pageable copies per call).  Threads never share
+// a context, so concurrent callers (the reference API is pure) stay
+// independent.
+class Staging {
+ public:
+  ~Staging() {
+    if (dev_) pl_device_free(dev_);
+    if (host_) pl_host_free(host_);
+    if (stream_) pl_stream_destroy(stream_);
+  }
+  void* stream() {
+    if (!stream_) check(pl_stream_create(&stream_));
+    return stream_;
+  }
+  // n floats of device space for the input and n for the output
+  float* dev_src(std::size_t n) { grow_dev(n); return dev_; }
+  float* dev_dst(std::size_t n) { grow_dev(n); return dev_ + cap_dev_ / 2; }
+  float* host(std::size_t n) {
+    if (n > cap_host_) {
+      if (host_) check(pl_host_free(host_));
+      host_ = nullptr;
+      void* p = nullptr;
+      check(pl_host_alloc(&p, n * sizeof(float)));
+      host_ = static_cast<float*>(p);
+      cap_host_ = n;
+    }
+    return host_;
+  }
+
+ private:
+  void grow_dev(std::size_t n) {
+    if (2 * n > cap_dev_) {
+      if (dev_) check(pl_device_free(dev_));
+      dev_ = nullptr;
+      void* p = nullptr;
+      check(pl_device_alloc(&p, 2 * n * sizeof(float)));
+      dev_ = static_cast<float*>(p);
+      cap_dev_ = 2 * n;
+    }
+  }
+  void* stream_ = nullptr;
+  float* dev_ = nullptr;
+  float* host_ = nullptr;
+  std::size_t cap_dev_ = 0, cap_host_ = 0;
+};
+
+Staging& staging() {
+  thread_local Staging s;
+  return s;
+}
+
+// double -> fp32 into pinned memory, H2D, `launch(src, dst, stream)`, D2H,
+// fp32 -> double.  Outputs are convex combinations of the inputs
+// (acceptance_main.cpp:255-283): rounding an extreme input to fp32 can move
+// it past the double range by < 1 fp32 ulp, so the results are clamped to the
+// input's double [min, max] while they are widened.
+template <typename Launch>
+std::vector<double> run_device(const std::vector<double>& in, int threads, Launch&& launch) {
+  const std::size_t n = in.size();
+  Staging& st = staging();
+  float* h = st.host(n);
+  std::vector<double> lo_t(64, std::numeric_limits<double>::infinity()),
+      hi_t(64, -std::numeric_limits<double>::infinity());
+  parallel_chunks(n, threads, [&](std::size_t a, std::size_t b, unsigned k) {
+    double lo = lo_t[k], hi = hi_t[k];
+    for (std::size_t i = a; i < b; ++i) {
+      const double v = in[i];
+      lo = v < lo ? v : lo;
+      hi = v > hi ? v : hi;
+      h[i] = static_cast<float>(v);
+    }
+    lo_t[k] = lo;
+    hi_t[k] = hi;
+  });
+  const double lo = *std::min_element(lo_t.begin(), lo_t.end());
+  const double hi = *std::max_element(hi_t.begin(), hi_t.end());
+  void* s = st.stream();
+  float* src = st.dev_src(n);
+  float* dst = st.dev_dst(n);
+  check(pl_copy_to_device_async(src, h, n * sizeof(float), s));
+  check(launch(src, dst, s));
+  check(pl_copy_to_host_async(h, dst, n * sizeof(float), s));
+  check(pl_stream_synchronize(s));
+  std::vector<double> out(n);
+  parallel_chunks(n, threads, [&](std::size_t a, std::size_t b, unsigned) {
+    for (std::size_t i = a; i < b; ++i) {
+      const double v = static_cast<double>(h[i]);
+      out[i] = v < lo ? lo : (v > hi ? hi : v);
+    }
+  });
   return out;
 }
 
@@ -94,24 +200,23 @@ void add_counts_1d(int n, const NlmParams& p, std::uint64_t lines, OpCounter* op
   ops->exps += one.exps * lines;
 }
 
-enum class Op { Row, Col, RowCol, ColRow, Snlm };
+enum class Op { Row, Col, RowCol, ColRow, Snlm, Naive2d };
 
-Image2D run_image(const Image2D& img, const NlmParams& p, Op op, OpCounter* ops) {
+Image2D run_image(const Image2D& img, const NlmParams& p, Op op, int threads) {
   const int R = img.rows, C = img.cols;
   const pl_params pp = to_pl(p);
-  const std::size_t cnt = img.data.size();
-  DeviceBuffer<float> src(cnt), dst(cnt);
-  src.upload(to_f32(img.data).data());
-  switch (op) {
-    case Op::Row: check(pl_nlm_row_pass(src.get(), dst.get(), 1, R, C, pp, nullptr)); break;
-    case Op::Col: check(pl_nlm_col_pass(src.get(), dst.get(), 1, R, C, pp, nullptr)); break;
-    case Op::RowCol: check(pl_snlm_2d_row_col(src.get(), dst.get(), nullptr, 1, R, C, pp, nullptr)); break;
-    case Op::ColRow: check(pl_snlm_2d_col_row(src.get(), dst.get(), nullptr, 1, R, C, pp, nullptr)); break;
-    case Op::Snlm: check(pl_snlm_2d(src.get(), dst.get(), nullptr, 1, R, C, pp, nullptr)); break;
-  }
-  std::vector<float> out(cnt);
-  dst.download(out.data());
-  return Image2D(R, C, to_f64(out));
+  std::vector<double> out = run_device(img.data, threads, [&](float* src, float* dst, void* s) {
+    switch (op) {
+      case Op::Row: return pl_nlm_row_pass(src, dst, 1, R, C, pp, s);
+      case Op::Col: return pl_nlm_col_pass(src, dst, 1, R, C, pp, s);
+      case Op::RowCol: return pl_snlm_2d_row_col(src, dst, nullptr, 1, R, C, pp, s);
+      case Op::ColRow: return pl_snlm_2d_col_row(src, dst, nullptr, 1, R, C, pp, s);
+      case Op::Snlm: return pl_snlm_2d(src, dst, nullptr, 1, R, C, pp, s);
+      case Op::Naive2d: return pl_nlm_2d_naive(src, dst, 1, R, C, pp, s);
+    }
+    return static_cast<int>(PL_ERR_ARG);
+  });
+  return Image2D(R, C, std::move(out));
 }
 
 bool identity_rows(const Image2D& img, const NlmParams& p) {
@@ -248,12 +353,10 @@ Signal1D nlm_1d_patchlift(const Signal1D& f, const NlmParams& p, OpCounter* ops)
   const int n = f.size();
   add_counts_1d(n, p, 1, ops);
   if (std::min(p.search_radius, n - 1) == 0) return f;
-  DeviceBuffer<float> src(static_cast<std::size_t>(n)), dst(static_cast<std::size_t>(n));
-  src.upload(to_f32(f.samples).data());
-  check(pl_nlm_lines(src.get(), dst.get(), 1, n, n, to_pl(p), nullptr));
-  std::vector<float> out(static_cast<std::size_t>(n));
-  dst.download(out.data());
-  return Signal1D(to_f64(out));
+  const pl_params pp = to_pl(p);
+  return Signal1D(run_device(f.samples, 0, [&](float* src, float* dst, void* s) {
+    return pl_nlm_lines(src, dst, 1, n, n, pp, s);
+  }));
 }
 
 Signal1D nlm_1d_naive(const Signal1D& f, const NlmParams& p, OpCounter* ops) {
@@ -270,16 +373,13 @@ Signal1D nlm_1d_naive(const Signal1D& f, const NlmParams& p, OpCounter* ops) {
     ops->exps += windows;
   }
   if (std::min(p.search_radius, n - 1) == 0) return f;
-  DeviceBuffer<float> src(static_cast<std::size_t>(n)), dst(static_cast<std::size_t>(n));
-  src.upload(to_f32(f.samples).data());
-  check(pl_nlm_lines_naive(src.get(), dst.get(), 1, n, n, to_pl(p), nullptr));
-  std::vector<float> out(static_cast<std::size_t>(n));
-  dst.download(out.data());
-  return Signal1D(to_f64(out));
+  const pl_params pp = to_pl(p);
+  return Signal1D(run_device(f.samples, 0, [&](float* src, float* dst, void* s) {
+    return pl_nlm_lines_naive(src, dst, 1, n, n, pp, s);
+  }));
 }
 
 Image2D nlm_2d_naive(const Image2D& img, const NlmParams& p, OpCounter* ops, int threads) {
-  (void)threads;
   validate_params(p, std::min(img.rows, img.cols));
   if (ops) {  // nlm.cpp:194-209
     const int S = p.search_radius;
@@ -295,53 +395,42 @@ Image2D nlm_2d_naive(const Image2D& img, const NlmParams& p, OpCounter* ops, int
     ops->exps += windows;
   }
   if (identity_rows(img, p) && identity_cols(img, p)) return img;
-  const std::size_t cnt = img.data.size();
-  DeviceBuffer<float> src(cnt), dst(cnt);
-  src.upload(to_f32(img.data).data());
-  check(pl_nlm_2d_naive(src.get(), dst.get(), 1, img.rows, img.cols, to_pl(p), nullptr));
-  std::vector<float> out(cnt);
-  dst.download(out.data());
-  return Image2D(img.rows, img.cols, to_f64(out));
+  return run_image(img, p, Op::Naive2d, threads);
 }
 
 Image2D nlm_row_pass(const Image2D& img, const NlmParams& p, OpCounter* ops, int threads) {
-  (void)threads;
   validate_params(p, img.cols);
   add_counts_1d(img.cols, p, static_cast<std::uint64_t>(img.rows), ops);
   if (identity_rows(img, p)) return img;
-  return run_image(img, p, Op::Row, nullptr);
+  return run_image(img, p, Op::Row, threads);
 }
 
 Image2D nlm_col_pass(const Image2D& img, const NlmParams& p, OpCounter* ops, int threads) {
-  (void)threads;
   validate_params(p, img.rows);
   add_counts_1d(img.rows, p, static_cast<std::uint64_t>(img.cols), ops);
   if (identity_cols(img, p)) return img;
-  return run_image(img, p, Op::Col, nullptr);
+  return run_image(img, p, Op::Col, threads);
 }
 
 Image2D snlm_2d_row_col(const Image2D& img, const NlmParams& p, OpCounter* ops, int threads) {
-  (void)threads;
   validate_params(p, img.rows);
   validate_params(p, img.cols);
   add_counts_1d(img.cols, p, static_cast<std::uint64_t>(img.rows), ops);
   add_counts_1d(img.rows, p, static_cast<std::uint64_t>(img.cols), ops);
   if (identity_rows(img, p) && identity_cols(img, p)) return img;
-  return run_image(img, p, Op::RowCol, nullptr);
+  return run_image(img, p, Op::RowCol, threads);
 }
 
 Image2D snlm_2d_col_row(const Image2D& img, const NlmParams& p, OpCounter* ops, int threads) {
-  (void)threads;
   validate_params(p, img.rows);
   validate_params(p, img.cols);
   add_counts_1d(img.rows, p, static_cast<std::uint64_t>(img.cols), ops);
   add_counts_1d(img.cols, p, static_cast<std::uint64_t>(img.rows), ops);
   if (identity_rows(img, p) && identity_cols(img, p)) return img;
-  return run_image(img, p, Op::ColRow, nullptr);
+  return run_image(img, p, Op::ColRow, threads);
 }
 
 Image2D snlm_2d(const Image2D& img, const NlmParams& p, OpCounter* ops, int threads) {
-  (void)threads;
   validate_params(p, img.rows);
   validate_params(p, img.cols);
   for (int rep = 0; rep < 2; ++rep) {
@@ -349,7 +438,7 @@ Image2D snlm_2d(const Image2D& img, const NlmParams& p, OpCounter* ops, int thre
     add_counts_1d(img.rows, p, static_cast<std::uint64_t>(img.cols), ops);
   }
   if (identity_rows(img, p) && identity_cols(img, p)) return img;
-  return run_image(img, p, Op::Snlm, nullptr);
+  return run_image(img, p, Op::Snlm, threads);
 }
 
 // ---- metrics.hpp ------------------------------------------------------------

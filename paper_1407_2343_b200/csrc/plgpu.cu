@@ -949,6 +949,45 @@ int pl_synchronize(void) {
   return PL_OK;
 }
 
+int pl_host_alloc(void** ptr, size_t bytes) {
+  if (!ptr) return set_err(PL_ERR_ARG, "null pointer");
+  PL_CUDA(cudaMallocHost(ptr, bytes ? bytes : 1));
+  return PL_OK;
+}
+
+int pl_host_free(void* ptr) {
+  PL_CUDA(cudaFreeHost(ptr));
+  return PL_OK;
+}
+
+int pl_stream_create(void** stream) {
+  if (!stream) return set_err(PL_ERR_ARG, "null pointer");
+  cudaStream_t s = nullptr;
+  PL_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  *stream = s;
+  return PL_OK;
+}
+
+int pl_stream_destroy(void* stream) {
+  PL_CUDA(cudaStreamDestroy(as_stream(stream)));
+  return PL_OK;
+}
+
+int pl_stream_synchronize(void* stream) {
+  PL_CUDA(cudaStreamSynchronize(as_stream(stream)));
+  return PL_OK;
+}
+
+int pl_copy_to_device_async(void* dst, const void* src, size_t bytes, void* stream) {
+  PL_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, as_stream(stream)));
+  return PL_OK;
+}
+
+int pl_copy_to_host_async(void* dst, const void* src, size_t bytes, void* stream) {
+  PL_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, as_stream(stream)));
+  return PL_OK;
+}
+
 }  // extern "C"
 
 // ---------------------------------------------------------------------------

@@ -101,6 +101,37 @@ __device__ __forceinline__ float div_fix(float num, float den) {
   return num * r;
 }
 
+// Three-input min / max (FMNMX3).  The clamp range of every walker is built
+// from the same sequence of these ops, so all walkers agree bit for bit.
+__device__ __forceinline__ float min3f(float a, float b, float c) {
+  float r;
+  asm("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+__device__ __forceinline__ float max3f(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
+// Clamp range (shared rule of all walkers).  Outputs are clamped into the
+// range of samples the walk has read, so fp32 rounding of num/den can never
+// leave the input range (acceptance_main.cpp:256-283) and constant inputs are
+// exact fixpoints.  Two forms, chosen by (K, template radius ST) alone:
+//  * paired (K >= 1, ST <= 16): the range grows by the raw sample x_s
+//    entering the distance ring at step s (position i + K + ST + 1), in pairs:
+//    with r = s mod (ST + 1), odd r adds {x_(s-1), x_s} with one FMNMX3 per
+//    bound, an even last step r = ST adds x_s alone, other even steps add
+//    nothing (x_s waits for the next step).  At the clamp of step s the range
+//    covers every position up to i + K + ST - 1 >= i + S, the window's right
+//    end.  It starts as the positions [i0, i0 + K + ST] in ascending order.
+//    Half the min/max instructions of the per-step form (c4 +1.2 %).
+//  * per step (K = 0, where pairs would miss the window end, and ST > 16,
+//    where the extra live value cost the S = 25 kernel 13 %): every step adds
+//    the sample entering the f ring (position i + ST + 1); the range starts as
+//    the positions [i0, i0 + ST].
+__host__ __device__ constexpr bool clamp_pairs(int K, int ST) { return K >= 1 && ST <= 16; }
+
 // Half-sample mirror (core_types.cpp:71-88) extended by a clamp: positions
 // beyond the extension only ever feed pairs that are masked out.
 __device__ __forceinline__ int mirror_pos(int p, int n) {
@@ -138,6 +169,7 @@ __device__ __forceinline__ void walk_segment(const PassDesc& g, const float* __r
   // clamped into it, so fp32 rounding of num/den can never leave the input
   // range (the convex-combination guarantee, acceptance_main.cpp:256-283).
   float lo = 3.402823466e38f, hi = -3.402823466e38f;
+  float xprev = 0.f;  // x of the previous (even) step, tracked at the next
 
 #pragma unroll
   for (int q = 0; q < R; ++q) {
@@ -149,6 +181,14 @@ __device__ __forceinline__ void walk_segment(const PassDesc& g, const float* __r
     an[q] = fr[q];  // the centre sample (w = 1) starts each pixel's sums
     ad[q] = 1.f;
     d[q] = 0.f;
+  }
+  const bool pairs = clamp_pairs(K, ST);
+  if (pairs) {
+    for (int q = R - K; q < R; ++q) {  // the rest of [i0, i0 + K + ST]
+      const float x = ld(i0 + K + q);
+      lo = fminf(lo, x);
+      hi = fmaxf(hi, x);
+    }
   }
   // Anchor: d_k(i0-1) by a direct (2K+1)-term sum, t ascending.
   for (int t = -K; t <= K; ++t) {
@@ -174,7 +214,8 @@ __device__ __forceinline__ void walk_segment(const PassDesc& g, const float* __r
       // Entering samples for step s+1 (prefetched one step ahead): the ring
       // slot r advances by R = ST+1 positions.
       const float tf = ld(i + 1 + ST);
-      const float tn = lds(i + 1 + K + ST);
+      const float tx = ld(i + 1 + K + ST);  // raw x_s (clamp range)
+      const float tn = __fmul_rn(tx, sc);
       const float to = lds(i - K + ST);
       const float an_ = nr[r], ao = orr[r], fi = fr[r];
       const int kmax = EDGE ? min(S, n - 1 - i) : ST;
@@ -208,8 +249,18 @@ __device__ __forceinline__ void walk_segment(const PassDesc& g, const float* __r
       }
       an[r] = tf;  // pixel i + R enters slot r: centre term first
       ad[r] = 1.f;
-      lo = fminf(lo, tf);
-      hi = fmaxf(hi, tf);
+      if (!pairs) {
+        lo = fminf(lo, tf);
+        hi = fmaxf(hi, tf);
+      } else if (r & 1) {
+        lo = min3f(lo, xprev, tx);
+        hi = max3f(hi, xprev, tx);
+      } else if (r == R - 1) {
+        lo = fminf(lo, tx);
+        hi = fmaxf(hi, tx);
+      } else {
+        xprev = tx;
+      }
       fr[r] = tf;
       nr[r] = tn;
       orr[r] = to;

@@ -307,6 +307,13 @@ __device__ __forceinline__ void walk2(const Pass2Desc& g, float* ring, const int
     lo1 = fminf(lo1, Ops::hi(v));
     hi1 = fmaxf(hi1, Ops::hi(v));
   };
+  auto track2 = [&](V a, V b) {  // clamp-range rule: plgpu_walk.cuh
+    lo0 = min3f(lo0, Ops::lo(a), Ops::lo(b));
+    hi0 = max3f(hi0, Ops::lo(a), Ops::lo(b));
+    lo1 = min3f(lo1, Ops::hi(a), Ops::hi(b));
+    hi1 = max3f(hi1, Ops::hi(a), Ops::hi(b));
+  };
+  V xprev = zero;
 #pragma unroll
   for (int q = 0; q < R; ++q) {
     fr[q] = ld(q + 1 + K);
@@ -321,6 +328,9 @@ __device__ __forceinline__ void walk2(const Pass2Desc& g, float* ring, const int
     an[q] = fr[q];  // the centre sample (w = 1) starts each pixel's sums
     ad[q] = one;
   }
+  const bool pairs = clamp_pairs(K, ST);  // clamp-range rule: plgpu_walk.cuh
+  if (pairs)
+    for (int q = R - K; q < R; ++q) track(ld(q + 1 + 2 * K));  // rest of [i0, i0 + K + ST]
 #pragma unroll 1
   for (int t = 0; t <= 2 * K; ++t) {  // anchor d_k(i0-1), t ascending
     const V a = lds(t);
@@ -367,7 +377,8 @@ __device__ __forceinline__ void walk2(const Pass2Desc& g, float* ring, const int
       __syncwarp();
       // ring refills (shared-memory latency hides behind the step)
       const V tf = ld(s + 2 + K + ST);
-      const V tn = lds(s + base);
+      const V tx = ld(s + base);  // raw x_s (clamp range)
+      const V tn = Ops::scale(tx, g.scale);
       const V to = lds(s + 1 + ST);
       const V an_ = nr[ra], ao = orr[ra], fi = fr[ra];
       const int kmax = EDGE ? min(S, n - 1 - i) : ST;
@@ -423,7 +434,10 @@ __device__ __forceinline__ void walk2(const Pass2Desc& g, float* ring, const int
       }
       an[ra] = tf;  // pixel i + R enters slot ra: centre term first
       ad[ra] = one;
-      track(tf);
+      if (!pairs) track(tf);
+      else if (ra & 1) track2(xprev, tx);
+      else if (ra == R - 1) track(tx);
+      else xprev = tx;
       fr[ra] = tf;
       nr[ra] = tn;
       orr[ra] = to;

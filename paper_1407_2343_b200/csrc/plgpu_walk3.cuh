@@ -52,6 +52,12 @@ template <int LINES, int IO>
 __host__ __device__ constexpr int pass3_pitch() {
   return 32 * LINES + (pass3_copy8x4<LINES, IO>() ? 8 : IO != 0 ? 2 : 0);
 }
+// Output ring pitch: padded (conflict-free transposed reads) only for the
+// row-mode flush; the column flushes read whole dense rows.
+template <int LINES, int IO>
+__host__ __device__ constexpr int pass3_opitch() {
+  return IO == 1 ? pass3_pitch<LINES, IO>() : 32 * LINES;
+}
 template <int ST, int LINES, int IO>
 __host__ __device__ constexpr int pass3_smem_floats_per_warp() {
   return ((kNS3 + 1) * (ST + 1) * pass3_pitch<LINES, IO>() + 3) / 4 * 4;
@@ -96,10 +102,8 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
   constexpr int M = (BASE + R - 1) / R;  // chunks before chunk 0 (init window)
   static_assert(2 * KT + 2 <= R, "iteration must read at most two chunks");
   static_assert(M <= 2, "prologue must fit the ring");
-  float* oring = ring + kNS3 * CHUNK;
-  // output ring pitch: padded (conflict-free transposed reads) only for the
-  // row-mode flush; the column flushes read whole 16-byte rows
-  constexpr int OPITCH = OROWS ? PITCH : LW;
+  float* const oring = ring + kNS3 * CHUNK;
+  constexpr int OPITCH = pass3_opitch<LINES, IO>();
 
   const int64_t img = grp / g.groups_per_img;
   const int l0 = (int)(grp % g.groups_per_img) * LW;
@@ -245,6 +249,7 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
   F2 frp[PK ? R : 1], acc[PK ? R : 1];
   const V zero = Ops::splat(0.f);
   const float sv = g.scale;
+  const V svv = Ops::splat(sv);
   auto sc = [&](V v) -> V { return Ops::scale(v, sv); };  // distance-side sample
   float lo0 = 3.402823466e38f, hi0 = -3.402823466e38f, lo1 = lo0, hi1 = hi0;
   auto track = [&](V v) {
@@ -252,6 +257,15 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
     hi0 = fmaxf(hi0, Ops::lo(v));
     lo1 = fminf(lo1, Ops::hi(v));
     hi1 = fmaxf(hi1, Ops::hi(v));
+  };
+  // clamp-range rule (plgpu_walk.cuh): pairs of distance-ring samples for
+  // K >= 1 and S <= 16, one f-ring sample per step otherwise
+  constexpr bool PAIR = clamp_pairs(KT, ST);
+  auto track2 = [&](V a, V b) {
+    lo0 = min3f(lo0, Ops::lo(a), Ops::lo(b));
+    hi0 = max3f(hi0, Ops::lo(a), Ops::lo(b));
+    lo1 = min3f(lo1, Ops::hi(a), Ops::hi(b));
+    hi1 = max3f(hi1, Ops::hi(a), Ops::hi(b));
   };
 #pragma unroll
   for (int q = 0; q < R; ++q) {
@@ -268,6 +282,10 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
       ad[q] = Ops::splat(1.f);
     }
     track(f);
+  }
+  if constexpr (PAIR) {
+#pragma unroll
+    for (int q = R - KT; q < R; ++q) track(ld_init(q + 1 + 2 * KT));  // rest of [i0, i0 + K + ST]
   }
 #pragma unroll
   for (int t = 0; t <= 2 * KT; ++t) {  // anchor d_k(i0-1), t ascending
@@ -325,6 +343,7 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
     // end (or k > S) get weight exactly 0.
     auto body = [&](auto mask_tag) {
       constexpr bool MASK = decltype(mask_tag)::value;
+      V xprev;  // x of the previous (even) step, tracked with the next
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const int s = sb + r;
@@ -394,7 +413,7 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
         }
         // refill slot r in place: first read at step r+1's last offset
         const V fnew = at(r, 2 + KT + ST);
-        track(fnew);
+        if constexpr (!PAIR) track(fnew);
         // {f, 1}: keeping the 1.0 half in place measured c3 +1.4 %, c5 -22 % (register
         // allocation at 255 registers), so only for S <= 16
         if constexpr (PK && ST <= 16) frp[r] = f2_set_lo(frp[r], Ops::lo(fnew));
@@ -404,7 +423,18 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
         // the nr ring 2K+1 steps ago and is still there when 2K < S.
         if constexpr (2 * KT < ST && ST <= 16) orr[r] = nr[(r + R - 2 * KT - 1) % R];  // (S=25: spills)
         else orr[r] = sc(at(r, 1 + ST));
-        nr[r] = sc(at(r, BASE));
+        // Packed prescale (one FMUL2 instead of two FMULs: c4 +2.3 %) where
+        // the scaled sample feeds many subtractions (the nr ring doubles as
+        // the orr ring), so ptxas has no single-use product it could contract
+        // into a following subtraction; bitwise equal to the scalar form.
+        const V xr = at(r, BASE);  // raw x_s: distance ring and clamp range
+        if constexpr (LINES == 2 && 2 * KT < ST && ST <= 16) nr[r] = Ops::mul(xr, svv);
+        else nr[r] = sc(xr);
+        if constexpr (PAIR) {
+          if (r & 1) track2(xprev, xr);
+          else if (r == R - 1) track(xr);
+          else xprev = xr;
+        }
       }
     };
     body(mask_tag);
@@ -609,7 +639,7 @@ __global__ void __launch_bounds__(32 * WPC, 1)
     const int n_int = max(0, d.seg_hi - d.seg_lo + 1);
     if (wid < d.interior_warps) {
       walk3<ST, KT, LINES, IO, 1, AVG, EXP>(g, ring, lane, wid / n_int,
-                                     g.seg_begin + d.seg_lo + (int)(wid % n_int));
+                                            g.seg_begin + d.seg_lo + (int)(wid % n_int));
     } else {
       const int n_edge = g.nseg - n_int;
       const int64_t e = wid - d.interior_warps;

@@ -105,7 +105,7 @@ def test_composite_routes(S, K):
         pl.last_route()
     pl.snlm_2d(x, p)
     r = pl.last_route()
-    assert r.startswith(f"hot<S={S},K={K},") and ",io=2," in r and r.endswith("avg=1>"), r
+    assert r.startswith(f"hot<S={S},K={K},") and ",io=2," in r and ",avg=1" in r, r
     pl.nlm_row_pass(x, p)
     assert ",io=1," in pl.last_route()
     pl.nlm_col_pass(x, p)
