@@ -85,6 +85,12 @@ const char* pl_last_error(void);
  * ("hot<S=..,K=..,lines=..,io=..,wpc=..,avg=..>", "staged<...>",
  * "portable<...>", "direct", "none"); for composites, their last pass. */
 const char* pl_last_route(void);
+/* Debug / test hook: pin the kernel route process-wide.  walker 0 = default,
+ * 1 = portable walker only, 2 = no hot-configuration kernel; lines 0/1/2 and
+ * wpc 0/2/8 pin the hot kernel's lines per lane and warps per CTA (0 =
+ * default).  Every route computes the same bits; this only selects code for
+ * coverage and A/B timing.  (0, 0, 0) restores the defaults. */
+int pl_debug_set_route(int32_t walker, int32_t lines, int32_t wpc);
 /* Name of the device the library will launch on, or "" if none. */
 const char* pl_device_name(void);
 

@@ -39,7 +39,7 @@ EXPORTS = [
     "pl_nlm_pass_strided", "pl_nlm_row_pass_fanout", "pl_last_route",
     "pl_debug_hot_distance_band", "pl_host_alloc", "pl_host_free", "pl_stream_create",
     "pl_stream_destroy", "pl_stream_synchronize", "pl_copy_to_device_async",
-    "pl_copy_to_host_async",
+    "pl_copy_to_host_async", "pl_debug_set_route",
 ]
 PL_MAX_FANOUT = 2
 
@@ -89,6 +89,7 @@ def lib() -> C.CDLL:
             "pl_abi_version": ([], C.c_int),
             "pl_last_error": ([], C.c_char_p),
             "pl_last_route": ([], C.c_char_p),
+            "pl_debug_set_route": ([i32, i32, i32], C.c_int),
             "pl_debug_hot_distance_band": ([vp, vp, i32, i32, i32, i32, vp], C.c_int),
             "pl_device_name": ([], C.c_char_p),
             "pl_validate_params": ([P, i32], C.c_int),
@@ -177,6 +178,22 @@ def _out(out, like, shape=None):
     if out.numel() != math.prod(shape):
         raise ValueError(f"out has {out.numel()} elements, expected {math.prod(shape)} {shape}")
     return out
+
+
+class debug_route:
+    """Context manager pinning the kernel route (pl_debug_set_route): walker 0
+    default / 1 portable only / 2 no hot kernel; lines, wpc of the hot kernel
+    (0 = default).  Results are bitwise identical on every route."""
+
+    def __init__(self, walker: int = 0, lines: int = 0, wpc: int = 0):
+        self.args = (int(walker), int(lines), int(wpc))
+
+    def __enter__(self):
+        _check(lib().pl_debug_set_route(*self.args))
+        return self
+
+    def __exit__(self, *a):
+        lib().pl_debug_set_route(0, 0, 0)
 
 
 def last_route() -> str:

@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
 #include <mutex>
 #include <string>
 
@@ -75,11 +76,13 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 // evenly over 2, 4 or 8 GPUs.  Signal-length lines (32768+ samples: 1D
 // signals, processed one or a few at a time) use ~64-sample segments so a
 // single line still spreads over enough threads: c1 (one 65,536-sample
-// line) 195 -> ~1,000 Msample/s on the B200 for S/64 extra pre-walk.
+// line) 195 -> ~1,000 Msample/s on the B200 for S/64 extra pre-walk.  Short
+// lines (<= 1024 samples: small images, a few hundred lines each) also use
+// ~64-sample segments, so a 512^2 image runs 64 warps instead of 16.
 int32_t segment_length(int32_t n, int32_t S) {
   const int32_t R = std::max(1, S + 1);
   // long segments: pre-walk overhead S/C stays small
-  const int32_t target = n >= 32768 ? 64 : 480;
+  const int32_t target = (n >= 32768 || n <= 1024) ? 64 : 480;
   int32_t nseg = std::max(1, (n + target - 1) / target);
   if (n >= 8192) nseg = std::max(8, (nseg + 4) / 8 * 8);
   int32_t C = (n + nseg - 1) / nseg;       // near-equal segments
@@ -88,43 +91,31 @@ int32_t segment_length(int32_t n, int32_t S) {
   return n < C ? n : C;
 }
 
-// Kernel selection: the production walker (plgpu_walk2.cuh) serves K <= 7 on
-// either axis; the portable walker (plgpu_walk.cuh, same arithmetic, bitwise
-// equal results) serves larger patch radii.  PLGPU_FORCE_WALKER=1 forces the
-// portable one (used by the tests to prove the two agree bit for bit).
-bool force_portable() {
-  static const bool f = [] {
-    const char* e = std::getenv("PLGPU_FORCE_WALKER");
-    return e && e[0] == '1';
-  }();
-  return f;
-}
+// Kernel selection: the hot-configuration kernel (plgpu_walk3.cuh) for the
+// configs' (K, S), the production walker (plgpu_walk2.cuh) for K <= 7 on
+// either axis, the portable walker (plgpu_walk.cuh) for larger patch radii;
+// all run the same per-line arithmetic (bitwise-equal results).  The routing
+// and the hot kernel's lines-per-lane / warps-per-CTA can be pinned for
+// testing through pl_debug_set_route (process-wide; performance and coverage
+// only -- no setting changes a result bit).  No environment variable is read.
+std::atomic<int> g_dbg_walker{0};  // 0 default, 1 portable only, 2 no hot kernel
+std::atomic<int> g_dbg_lines{0};   // 0 default, 1 or 2 lines per lane (S <= 16)
+std::atomic<int> g_dbg_wpc{0};     // 0 default, 2 or 8 warps per CTA
+
+bool force_portable() { return g_dbg_walker.load(std::memory_order_relaxed) == 1; }
+bool force_portable_v2() { return g_dbg_walker.load(std::memory_order_relaxed) == 2; }
 // Lines per lane of the hot-configuration kernel: 1 = one line per lane with
 // {num, den} packed, 2 = two lines per lane packed line-wise.
 int walk3_lines(int ST) {
-  static const int forced = [] {
-    const char* e = std::getenv("PLGPU_LINES");
-    return (e && (e[0] == '1' || e[0] == '2')) ? e[0] - '0' : 0;
-  }();
   if (ST > 16) return 1;
-  if (forced) return forced;
+  const int forced = g_dbg_lines.load(std::memory_order_relaxed);
+  if (forced == 1 || forced == 2) return forced;
   return ST <= 10 ? 2 : 1;  // measured on B200: c4 (S=10) 2 lines, c3 (S=15) 1 line
 }
 int walk3_wpc(int ST) {
-  static const int forced = [] {
-    const char* e = std::getenv("PLGPU_WPC");
-    return e ? std::atoi(e) : 0;
-  }();
+  const int forced = g_dbg_wpc.load(std::memory_order_relaxed);
   if (forced == 2 || forced == 8) return forced;
   return ST >= 15 ? 8 : 2;  // measured: lockstep helps S=15/25 (I-cache), hurts S=10
-}
-// PLGPU_FORCE_WALKER=2 skips only the hot-configuration kernel (walk3).
-bool force_portable_v2() {
-  static const bool f = [] {
-    const char* e = std::getenv("PLGPU_FORCE_WALKER");
-    return e && e[0] == '2';
-  }();
-  return f;
 }
 
 // Largest radius with a specialised walker; larger radii use the direct kernel.
@@ -488,6 +479,16 @@ int distance_band(const float* src, T* band, int64_t n_lines, int32_t n, int64_t
 extern "C" {
 
 int pl_abi_version(void) { return PLGPU_ABI_VERSION; }
+
+int pl_debug_set_route(int32_t walker, int32_t lines, int32_t wpc) {
+  if (walker < 0 || walker > 2 || (lines != 0 && lines != 1 && lines != 2) ||
+      (wpc != 0 && wpc != 2 && wpc != 8))
+    return set_err(PL_ERR_ARG, "debug route: walker 0..2, lines 0/1/2, wpc 0/2/8");
+  g_dbg_walker.store(walker);
+  g_dbg_lines.store(lines);
+  g_dbg_wpc.store(wpc);
+  return PL_OK;
+}
 
 const char* pl_last_error(void) { return g_err.c_str(); }
 

@@ -375,70 +375,53 @@ def test_cpp_dropin_library():
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
 
 
-def test_hot_kernel_line_modes_bitwise(tmp_path):
-    """PLGPU_LINES / PLGPU_WPC pick the hot kernel's lines per lane and warps
-    per CTA (performance knobs only): every combination, with every staging /
-    flush mode (row pass, column pass, transposed-intermediate RC, S-NLM with
-    the fused average), gives the same bits."""
-    import os
-    import subprocess
-    import sys
-    code = (
-        "import sys, numpy as np, torch; sys.path.insert(0, %r)\n"
-        "import paper_1407_2343_b200 as pl\n"
-        "rng = np.random.default_rng(8)\n"
-        "outs = {}\n"
-        "for (b, r, c, S, K) in [(2, 200, 256, 10, 3), (1, 130, 192, 15, 5), (1, 120, 96, 25, 7)]:\n"
-        "    x = torch.from_numpy(rng.uniform(0, 255, (b, r, c)).astype(np.float32)).cuda()\n"
-        "    p = (S, K, 40.0 + 5 * S)\n"
-        "    for nm, f in (('row', pl.nlm_row_pass), ('col', pl.nlm_col_pass),\n"
-        "                  ('rc', pl.snlm_2d_row_col), ('snlm', pl.snlm_2d)):\n"
-        "        outs[f'{S}_{nm}'] = f(x, p).cpu().numpy()\n"
-        "np.savez(sys.argv[1], **outs)\n" % os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-    files = []
-    for env_extra in ({}, {"PLGPU_LINES": "1"}, {"PLGPU_LINES": "2"}, {"PLGPU_WPC": "8"},
-                      {"PLGPU_WPC": "2"}, {"PLGPU_LINES": "1", "PLGPU_WPC": "8"}):
-        f = str(tmp_path / f"o{len(files)}.npz")
-        r = subprocess.run([sys.executable, "-c", code, f], env=dict(os.environ, **env_extra),
-                           capture_output=True, text=True, timeout=600)
-        assert r.returncode == 0, (env_extra, r.stderr[-3000:])
-        files.append(np.load(f))
-    for other in files[1:]:
-        for key in files[0].files:
-            assert np.array_equal(files[0][key], other[key]), key
+def test_hot_kernel_line_modes_bitwise():
+    """The hot kernel's lines per lane and warps per CTA (performance choices,
+    pinned through pl_debug_set_route): every combination, with every staging
+    / flush mode (row pass, column pass, transposed-intermediate RC, S-NLM
+    with the fused average), gives the same bits."""
+    rng = np.random.default_rng(8)
+    cases = [(2, 200, 256, 10, 3), (1, 130, 192, 15, 5), (1, 120, 96, 25, 7)]
+    xs = [dev(rng.uniform(0, 255, (b, r, c))) for (b, r, c, S, K) in cases]
+    runs = []
+    for lines, wpc in ((0, 0), (1, 0), (2, 0), (0, 8), (0, 2), (1, 8)):
+        outs = {}
+        with pl.debug_route(0, lines, wpc):
+            for x, (b, r, c, S, K) in zip(xs, cases):
+                p = (S, K, 40.0 + 5 * S)
+                for nm, f in (("row", pl.nlm_row_pass), ("col", pl.nlm_col_pass),
+                              ("rc", pl.snlm_2d_row_col), ("snlm", pl.snlm_2d)):
+                    outs[f"{S}_{nm}"] = host(f(x, p))
+                    assert pl.last_route().startswith("hot<"), pl.last_route()
+        runs.append(outs)
+    for other in runs[1:]:
+        for key in runs[0]:
+            assert np.array_equal(runs[0][key], other[key]), key
 
 
-def test_portable_and_production_walkers_bitwise_equal(tmp_path):
-    """The production walker (smem-staged, packed f32x2) and the portable one
-    (plgpu_walk.cuh) run the same per-line arithmetic: outputs are bitwise equal."""
-    import os
-    import subprocess
-    import sys
-    code = (
-        "import sys, numpy as np, torch; sys.path.insert(0, %r)\n"
-        "import paper_1407_2343_b200 as pl\n"
-        "rng = np.random.default_rng(5)\n"
-        "outs = {}\n"
-        "for (b, r, c, S, K) in [(2, 300, 517, 10, 3), (1, 260, 700, 15, 5), (1, 333, 290, 25, 7),"
-        " (3, 64, 128, 4, 2), (1, 40, 1000, 32, 7), (2, 1100, 96, 10, 3), (1, 70, 1500, 15, 5),"
-        " (1, 900, 100, 25, 7), (1, 7, 3000, 10, 3), (1, 40, 9000, 25, 7), (1, 1700, 64, 25, 7),"
-        " (1, 64, 2000, 15, 5), (1, 1600, 96, 15, 5), (1, 33, 16384, 25, 7)]:\n"
-        "    x = torch.from_numpy(rng.uniform(0, 255, (b, r, c)).astype(np.float32)).cuda()\n"
-        "    p = (S, K, 50.0 + 10 * S)\n"
-        "    outs[f'{r}x{c}_rc'] = pl.snlm_2d_row_col(x, p).cpu().numpy()\n"
-        "    outs[f'{r}x{c}_cr'] = pl.snlm_2d_col_row(x, p).cpu().numpy()\n"
-        "np.savez(sys.argv[1], **outs)\n" % os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-    files = []
-    for force in ("0", "1", "2"):  # production(walk3/walk2), portable, walk2 only
-        f = str(tmp_path / f"out{force}.npz")
-        env = dict(os.environ, PLGPU_FORCE_WALKER=force)
-        r = subprocess.run([sys.executable, "-c", code, f], env=env, capture_output=True, text=True,
-                           timeout=600)
-        assert r.returncode == 0, r.stderr[-3000:]
-        files.append(np.load(f))
-    for key in files[0].files:
-        assert np.array_equal(files[0][key], files[1][key]), key
-        assert np.array_equal(files[0][key], files[2][key]), key
+def test_portable_and_production_walkers_bitwise_equal():
+    """The hot kernel (walk3), the production walker (smem-staged, packed
+    f32x2, walk2) and the portable one (plgpu_walk.cuh) run the same per-line
+    arithmetic: outputs are bitwise equal."""
+    rng = np.random.default_rng(5)
+    cases = [(2, 300, 517, 10, 3), (1, 260, 700, 15, 5), (1, 333, 290, 25, 7),
+             (3, 64, 128, 4, 2), (1, 40, 1000, 32, 7), (2, 1100, 96, 10, 3), (1, 70, 1500, 15, 5),
+             (1, 900, 100, 25, 7), (1, 7, 3000, 10, 3), (1, 40, 9000, 25, 7), (1, 1700, 64, 25, 7),
+             (1, 64, 2000, 15, 5), (1, 1600, 96, 15, 5), (1, 33, 16384, 25, 7), (1, 96, 300, 12, 0),
+             (2, 50, 1030, 8, 1)]
+    xs = [dev(rng.uniform(0, 255, (b, r, c))) for (b, r, c, S, K) in cases]
+    runs = []
+    for walker in (0, 1, 2):  # default (walk3/walk2), portable only, walk2 (no hot kernel)
+        outs = {}
+        with pl.debug_route(walker):
+            for x, (b, r, c, S, K) in zip(xs, cases):
+                p = (S, K, 50.0 + 10 * S)
+                outs[f"{r}x{c}_rc"] = host(pl.snlm_2d_row_col(x, p))
+                outs[f"{r}x{c}_cr"] = host(pl.snlm_2d_col_row(x, p))
+        runs.append(outs)
+    for key in runs[0]:
+        assert np.array_equal(runs[0][key], runs[1][key]), key
+        assert np.array_equal(runs[0][key], runs[2][key]), key
 
 
 def test_slab_transpose_emulated_bitwise():
