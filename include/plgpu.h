@@ -195,6 +195,16 @@ int pl_snlm_2d(const float* src, float* dst, float* work, int32_t batch, int32_t
 int pl_snlm_2d_row_col_host(const float* host_src, float* host_dst, int32_t batch, int32_t rows,
                             int32_t cols, pl_params p, void* stream);
 
+/* CUDA Graph of pl_snlm_2d_row_col on fixed buffers: both passes are captured
+ * once (the intermediate is owned by the graph when `work` is NULL) and each
+ * pl_graph_launch replays them with one launch on `stream`.  For repeated
+ * calls on small images, where launch latency is the cost. */
+typedef struct pl_graph pl_graph;
+int pl_graph_rc_create(const float* src, float* dst, float* work, int32_t batch, int32_t rows,
+                       int32_t cols, pl_params p, pl_graph** out);
+int pl_graph_launch(pl_graph* graph, void* stream);
+int pl_graph_destroy(pl_graph* graph);
+
 /* ---- classical 2D NLM (nlm_2d_naive, nlm.cpp:168-213): the baseline the
  * separable filter is compared against (per-pixel (2S+1)^2 window, direct
  * (2K+1)^2 patch distances, 2D half-sample mirror).  Not the hot path. */

@@ -39,7 +39,8 @@ EXPORTS = [
     "pl_nlm_pass_strided", "pl_nlm_row_pass_fanout", "pl_last_route",
     "pl_debug_hot_distance_band", "pl_host_alloc", "pl_host_free", "pl_stream_create",
     "pl_stream_destroy", "pl_stream_synchronize", "pl_copy_to_device_async",
-    "pl_copy_to_host_async", "pl_debug_set_route",
+    "pl_copy_to_host_async", "pl_debug_set_route", "pl_graph_rc_create", "pl_graph_launch",
+    "pl_graph_destroy",
 ]
 PL_MAX_FANOUT = 2
 
@@ -90,6 +91,9 @@ def lib() -> C.CDLL:
             "pl_last_error": ([], C.c_char_p),
             "pl_last_route": ([], C.c_char_p),
             "pl_debug_set_route": ([i32, i32, i32], C.c_int),
+            "pl_graph_rc_create": ([vp, vp, vp, i32, i32, i32, P, C.POINTER(vp)], C.c_int),
+            "pl_graph_launch": ([vp, vp], C.c_int),
+            "pl_graph_destroy": ([vp], C.c_int),
             "pl_debug_hot_distance_band": ([vp, vp, i32, i32, i32, i32, vp], C.c_int),
             "pl_device_name": ([], C.c_char_p),
             "pl_validate_params": ([P, i32], C.c_int),
@@ -397,6 +401,31 @@ def nlm_pass_strided(src, dst, batch: int, lines: int, n: int, src_line_stride: 
 
 def workspace_bytes(op: int, batch: int, rows: int, cols: int) -> int:
     return int(lib().pl_workspace_bytes(op, batch, rows, cols))
+
+
+class RCGraph:
+    """pl_snlm_2d_row_col captured as a CUDA Graph on fixed device buffers x ->
+    out; ``launch()`` replays both passes with one launch on the current
+    stream."""
+
+    def __init__(self, x, p, out=None):
+        import torch
+        _dev(x, torch.float32)
+        b, r, c = _image_dims(x)
+        self.x, self.out = x, _out(out, x)
+        h = C.c_void_p()
+        _check(lib().pl_graph_rc_create(x.data_ptr(), self.out.data_ptr(), None, b, r, c,
+                                        _params(p), C.byref(h)))
+        self._h = h
+
+    def launch(self):
+        _check(lib().pl_graph_launch(self._h, _stream(self.x)))
+        return self.out
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _LIB is not None:
+            _LIB.pl_graph_destroy(self._h)
+            self._h = None
 
 
 def snlm_2d_row_col_host(x_host, p, out_host=None):

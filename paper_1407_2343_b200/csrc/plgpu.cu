@@ -753,6 +753,79 @@ int pl_snlm_2d_row_col(const float* src, float* dst, float* work, int32_t batch,
   return rc_passes(src, dst, work, batch, rows, cols, p, as_stream(stream));
 }
 
+// ---- CUDA Graph of the RC composite ----------------------------------------
+// Both passes captured once on a private stream (the intermediate owned by the
+// graph unless the caller passes `work`); each pl_graph_launch replays them
+// with one launch call.  For repeated small calls (c2-sized images) the two
+// kernel launches and the scratch allocation leave the per-call path.
+struct pl_graph {
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  float* owned = nullptr;
+};
+
+int pl_graph_rc_create(const float* src, float* dst, float* work, int32_t batch, int32_t rows,
+                       int32_t cols, pl_params p, pl_graph** out) {
+  if (!out) return set_err(PL_ERR_ARG, "null graph handle");
+  *out = nullptr;
+  int rc = validate_image(batch, rows, cols);
+  if (!rc) rc = validate_params(p, rows);
+  if (!rc) rc = validate_params(p, cols);
+  if (!rc) rc = check_ptrs(src, dst);
+  if (rc) return rc;
+  pl_graph* g = new pl_graph();
+  auto fail = [&](int code) {
+    if (g->exec) cudaGraphExecDestroy(g->exec);
+    if (g->graph) cudaGraphDestroy(g->graph);
+    if (g->owned) cudaFree(g->owned);
+    delete g;
+    return code;
+  };
+  if (!work) {
+    cudaError_t e = cudaMalloc(&g->owned, std::max<size_t>(16, pl_workspace_bytes(0, batch, rows, cols)));
+    if (e != cudaSuccess) return fail(set_err(PL_ERR_CUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e)));
+    work = g->owned;
+  }
+  cudaStream_t st = nullptr;
+  cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  if (e != cudaSuccess) return fail(set_err(PL_ERR_CUDA, std::string("cudaStreamCreate: ") + cudaGetErrorString(e)));
+  e = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
+  if (e == cudaSuccess) {
+    rc = rc_passes(src, dst, work, batch, rows, cols, p, st);
+    cudaGraph_t graph = nullptr;
+    const cudaError_t e2 = cudaStreamEndCapture(st, &graph);
+    g->graph = graph;
+    if (!rc && e2 != cudaSuccess)
+      rc = set_err(PL_ERR_CUDA, std::string("cudaStreamEndCapture: ") + cudaGetErrorString(e2));
+  } else {
+    rc = set_err(PL_ERR_CUDA, std::string("cudaStreamBeginCapture: ") + cudaGetErrorString(e));
+  }
+  cudaStreamDestroy(st);
+  if (rc) return fail(rc);
+  e = cudaGraphInstantiate(&g->exec, g->graph, 0);
+  if (e != cudaSuccess)
+    return fail(set_err(PL_ERR_CUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(e)));
+  *out = g;
+  return PL_OK;
+}
+
+int pl_graph_launch(pl_graph* g, void* stream) {
+  if (!g || !g->exec) return set_err(PL_ERR_ARG, "null graph");
+  PL_CUDA(cudaGraphLaunch(g->exec, as_stream(stream)));
+  return PL_OK;
+}
+
+int pl_graph_destroy(pl_graph* g) {
+  if (!g) return PL_OK;
+  cudaError_t e = cudaSuccess;
+  if (g->exec) e = cudaGraphExecDestroy(g->exec);
+  if (g->graph) cudaGraphDestroy(g->graph);
+  if (g->owned) cudaFree(g->owned);
+  delete g;
+  if (e != cudaSuccess) return set_err(PL_ERR_CUDA, std::string("cudaGraphExecDestroy: ") + cudaGetErrorString(e));
+  return PL_OK;
+}
+
 int pl_snlm_2d_col_row(const float* src, float* dst, float* work, int32_t batch, int32_t rows,
                        int32_t cols, pl_params p, void* stream) {
   int rc = validate_image(batch, rows, cols);

@@ -421,7 +421,10 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
         else fr[r] = fnew;
         // The leaving-term partner entering now (coordinate s+1+ST) entered
         // the nr ring 2K+1 steps ago and is still there when 2K < S.
-        if constexpr (2 * KT < ST && ST <= 16) orr[r] = nr[(r + R - 2 * KT - 1) % R];  // (S=25: spills)
+        // The leaving partner entering now is copied from the nr ring (2-line
+        // kernel) or re-read from the staged chunk and scaled (1-line kernels:
+        // the copy's register shuffles cost c3 2.5 %; S = 25 spills with it).
+        if constexpr (2 * KT < ST && ST <= 16 && LINES == 2) orr[r] = nr[(r + R - 2 * KT - 1) % R];
         else orr[r] = sc(at(r, 1 + ST));
         // Packed prescale (one FMUL2 instead of two FMULs: c4 +2.3 %) where
         // the scaled sample feeds many subtractions (the nr ring doubles as

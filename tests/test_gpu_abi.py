@@ -184,3 +184,19 @@ def test_host_pipeline_reports_errors():
     returns the reference's message."""
     with pytest.raises(pl.ValidationError):
         pl.snlm_2d_row_col_host(np.zeros((4, 4), np.float32), (10, 9, 50.0))
+
+
+def test_rc_graph_replay_bitwise():
+    """pl_graph_rc_create / pl_graph_launch: the captured RC replays to the same
+    bits as the direct call, and sees new input values written in place."""
+    rng = np.random.default_rng(77)
+    x = dev(rng.uniform(0, 255, (2, 96, 160)))
+    p = (10, 3, 60.0)
+    g = pl.RCGraph(x, p)
+    torch.cuda.synchronize()
+    for t in range(3):
+        x.copy_(dev(rng.uniform(0, 255, (2, 96, 160))))
+        y = g.launch()
+        want = pl.snlm_2d_row_col(x, p)
+        torch.cuda.synchronize()
+        assert torch.equal(y, want), t
