@@ -812,24 +812,33 @@ def run_ours(args):
 
 def dropin_e2e(img, S, K, h, calls):
     """Mpixel/s through the C++ drop-in a reference caller links
-    (patchlift::snlm_2d_row_col on a double Image2D, threads=0: conversions,
-    copies and both passes per call), one image of the workload per call."""
+    (patchlift::snlm_2d_row_col on a double Image2D, threads=0: copies and both
+    passes per call), one image of the workload per call: its default
+    reference-precision fp64 route, and the fp32 route (conversions included)."""
     import tempfile
     exe = os.path.join(ROOT, "paper_1407_2343_b200", "lib", "dropin_bench")
     if not os.path.exists(exe):
         return {"unavailable": "lib/dropin_bench not built"}
+    res = {}
     with tempfile.NamedTemporaryFile(suffix=".f32") as f:
         np.ascontiguousarray(img, dtype=np.float32).tofile(f.name)
-        r = subprocess.run([exe, f.name, str(img.shape[0]), str(img.shape[1]), str(S), str(K),
-                            repr(float(h)), str(max(1, calls)), "0"],
-                           capture_output=True, text=True, timeout=600)
-    if r.returncode != 0:
-        return {"unavailable": (r.stderr or r.stdout).strip()[-300:]}
-    out = json.loads(r.stdout.strip().splitlines()[-1])
-    return {"value": out["mpx_s"], "unit": UNIT, "s_per_call": out["s_per_call"],
-            "calls": out["calls"], "images_per_call": 1,
+        for prec in ("fp64", "fp32"):
+            r = subprocess.run([exe, f.name, str(img.shape[0]), str(img.shape[1]), str(S), str(K),
+                                repr(float(h)), str(max(1, calls)), "0", prec],
+                               capture_output=True, text=True, timeout=600)
+            if r.returncode != 0:
+                res[prec] = {"unavailable": (r.stderr or r.stdout).strip()[-300:]}
+                continue
+            out = json.loads(r.stdout.strip().splitlines()[-1])
+            res[prec] = {"value": out["mpx_s"], "s_per_call": out["s_per_call"]}
+    line = {"value": res.get("fp64", {}).get("value"), "unit": UNIT, "calls": max(1, calls),
+            "images_per_call": 1, "precision": "fp64 (drop-in default)",
+            "fp32_route": res.get("fp32"),
             "api": "patchlift::snlm_2d_row_col (C++ drop-in, double Image2D in and out, "
                    "threads=0; tests/cpp/dropin_bench.cpp)"}
+    if "unavailable" in res.get("fp64", {}):
+        line["unavailable"] = res["fp64"]["unavailable"]
+    return line
 
 
 def arm_config(cfg_name, world):

@@ -211,6 +211,29 @@ int pl_graph_destroy(pl_graph* graph);
 int pl_nlm_2d_naive(const float* src, float* dst, int32_t batch, int32_t rows, int32_t cols,
                     pl_params p, void* stream);
 
+/* ---- fp64 reference-precision route (plgpu_walk64.cuh): the same filters on
+ * device DOUBLE buffers, in double arithmetic with exp(-d/(h*h)) -- outputs
+ * match the reference library (all-double, core_types.hpp:23,35) to rounding
+ * rather than to the fp32 tiers.  The C++ drop-in uses this route by default.
+ * `work` (or NULL for stream-ordered scratch) holds 2 * pl_workspace_bytes(op,
+ * ...) bytes (doubles). */
+int pl_nlm_lines_f64(const double* src, double* dst, int64_t n_lines, int32_t n, int64_t ld,
+                     pl_params p, void* stream);
+int pl_nlm_lines_naive_f64(const double* src, double* dst, int64_t n_lines, int32_t n, int64_t ld,
+                           pl_params p, void* stream);
+int pl_nlm_row_pass_f64(const double* src, double* dst, int32_t batch, int32_t rows, int32_t cols,
+                        pl_params p, void* stream);
+int pl_nlm_col_pass_f64(const double* src, double* dst, int32_t batch, int32_t rows, int32_t cols,
+                        pl_params p, void* stream);
+int pl_snlm_2d_row_col_f64(const double* src, double* dst, double* work, int32_t batch,
+                           int32_t rows, int32_t cols, pl_params p, void* stream);
+int pl_snlm_2d_col_row_f64(const double* src, double* dst, double* work, int32_t batch,
+                           int32_t rows, int32_t cols, pl_params p, void* stream);
+int pl_snlm_2d_f64(const double* src, double* dst, double* work, int32_t batch, int32_t rows,
+                   int32_t cols, pl_params p, void* stream);
+int pl_nlm_2d_naive_f64(const double* src, double* dst, int32_t batch, int32_t rows, int32_t cols,
+                        pl_params p, void* stream);
+
 /* ---- device memory helpers so host layers need no CUDA runtime of their own */
 int pl_device_alloc(void** ptr, size_t bytes);
 int pl_device_free(void* ptr);

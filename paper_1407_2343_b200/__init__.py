@@ -40,7 +40,9 @@ EXPORTS = [
     "pl_debug_hot_distance_band", "pl_host_alloc", "pl_host_free", "pl_stream_create",
     "pl_stream_destroy", "pl_stream_synchronize", "pl_copy_to_device_async",
     "pl_copy_to_host_async", "pl_debug_set_route", "pl_graph_rc_create", "pl_graph_launch",
-    "pl_graph_destroy",
+    "pl_graph_destroy", "pl_nlm_lines_f64", "pl_nlm_lines_naive_f64", "pl_nlm_row_pass_f64",
+    "pl_nlm_col_pass_f64", "pl_snlm_2d_row_col_f64", "pl_snlm_2d_col_row_f64", "pl_snlm_2d_f64",
+    "pl_nlm_2d_naive_f64",
 ]
 PL_MAX_FANOUT = 2
 
@@ -94,6 +96,14 @@ def lib() -> C.CDLL:
             "pl_graph_rc_create": ([vp, vp, vp, i32, i32, i32, P, C.POINTER(vp)], C.c_int),
             "pl_graph_launch": ([vp, vp], C.c_int),
             "pl_graph_destroy": ([vp], C.c_int),
+            "pl_nlm_lines_f64": ([vp, vp, i64, i32, i64, P, vp], C.c_int),
+            "pl_nlm_lines_naive_f64": ([vp, vp, i64, i32, i64, P, vp], C.c_int),
+            "pl_nlm_row_pass_f64": ([vp, vp, i32, i32, i32, P, vp], C.c_int),
+            "pl_nlm_col_pass_f64": ([vp, vp, i32, i32, i32, P, vp], C.c_int),
+            "pl_snlm_2d_row_col_f64": ([vp, vp, vp, i32, i32, i32, P, vp], C.c_int),
+            "pl_snlm_2d_col_row_f64": ([vp, vp, vp, i32, i32, i32, P, vp], C.c_int),
+            "pl_snlm_2d_f64": ([vp, vp, vp, i32, i32, i32, P, vp], C.c_int),
+            "pl_nlm_2d_naive_f64": ([vp, vp, i32, i32, i32, P, vp], C.c_int),
             "pl_debug_hot_distance_band": ([vp, vp, i32, i32, i32, i32, vp], C.c_int),
             "pl_device_name": ([], C.c_char_p),
             "pl_validate_params": ([P, i32], C.c_int),
@@ -401,6 +411,31 @@ def nlm_pass_strided(src, dst, batch: int, lines: int, n: int, src_line_stride: 
 
 def workspace_bytes(op: int, batch: int, rows: int, cols: int) -> int:
     return int(lib().pl_workspace_bytes(op, batch, rows, cols))
+
+
+def filter_f64(op: str, x, p):
+    """The fp64 reference-precision route on a float64 device tensor: op in
+    lines, lines_naive (x [..., n]), row, col, rc, cr, snlm, nlm2d (x [rows,
+    cols] or [batch, rows, cols])."""
+    import torch
+    _dev(x, torch.float64)
+    out = torch.empty_like(x)
+    L = lib()
+    if op in ("lines", "lines_naive"):
+        n = x.shape[-1]
+        fn = L.pl_nlm_lines_f64 if op == "lines" else L.pl_nlm_lines_naive_f64
+        _check(fn(x.data_ptr(), out.data_ptr(), x.numel() // n, n, n, _params(p), _stream(x)))
+        return out
+    b, r, c = _image_dims(x)
+    if op in ("rc", "cr", "snlm"):
+        fn = {"rc": L.pl_snlm_2d_row_col_f64, "cr": L.pl_snlm_2d_col_row_f64,
+              "snlm": L.pl_snlm_2d_f64}[op]
+        _check(fn(x.data_ptr(), out.data_ptr(), None, b, r, c, _params(p), _stream(x)))
+    else:
+        fn = {"row": L.pl_nlm_row_pass_f64, "col": L.pl_nlm_col_pass_f64,
+              "nlm2d": L.pl_nlm_2d_naive_f64}[op]
+        _check(fn(x.data_ptr(), out.data_ptr(), b, r, c, _params(p), _stream(x)))
+    return out
 
 
 class RCGraph:

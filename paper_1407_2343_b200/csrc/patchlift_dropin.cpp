@@ -7,8 +7,11 @@
 //    messages (core_types.cpp:13-98).
 //  * Every filter and compute_banded_kernel run on the device.  There is no
 //    CPU route: if the device library fails, the call throws.
-//  * Precision: images/signals are converted double -> fp32 for the device and
-//    back (documented re-tiering).  When the effective
+//  * Precision: by default every filter runs the fp64 kernels on the device
+//    (plgpu_walk64.cuh: double in, double arithmetic, double out), so results
+//    match the reference to rounding; set_device_precision(fast_fp32)
+//    (include/patchlift/b200.hpp) selects the fp32 throughput kernels instead
+//    (double -> fp32 -> double, DESIGN.md sec. 5 tiers).  When the effective
 //    search radius is 0 the filter is the identity and the input is returned
 //    bit for bit (nlm_test.cpp:87-99).
 //  * OpCounter receives the reference's closed forms (pl_op_counts_1d).
@@ -17,8 +20,10 @@
 //    threads, nlm.cpp:18-54) parallelises the host-side double <-> fp32
 //    conversions.  Results do not depend on it, as upstream (nlm.cpp:13-17).
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstring>
 #include <limits>
 #include <memory>
 #include <ostream>
@@ -28,6 +33,7 @@
 #include <thread>
 #include <vector>
 
+#include "patchlift/b200.hpp"
 #include "patchlift/banded_kernel.hpp"
 #include "patchlift/core_types.hpp"
 #include "patchlift/metrics.hpp"
@@ -105,36 +111,44 @@ class Staging {
     if (!stream_) check(pl_stream_create(&stream_));
     return stream_;
   }
-  // n floats of device space for the input and n for the output
-  float* dev_src(std::size_t n) { grow_dev(n); return dev_; }
-  float* dev_dst(std::size_t n) { grow_dev(n); return dev_ + cap_dev_ / 2; }
-  float* host(std::size_t n) {
-    if (n > cap_host_) {
+  // Device space for an input and an output of `bytes` each (+ `work_bytes`
+  // of composite scratch), and pinned host space of `bytes`.
+  void* dev_src(std::size_t bytes, std::size_t work_bytes = 0) {
+    grow_dev(bytes, work_bytes);
+    return dev_;
+  }
+  void* dev_dst() { return dev_ + half_; }
+  void* dev_work() { return dev_ + 2 * half_; }
+  void* host(std::size_t bytes) {
+    if (bytes > cap_host_) {
       if (host_) check(pl_host_free(host_));
       host_ = nullptr;
       void* p = nullptr;
-      check(pl_host_alloc(&p, n * sizeof(float)));
-      host_ = static_cast<float*>(p);
-      cap_host_ = n;
+      check(pl_host_alloc(&p, bytes));
+      host_ = static_cast<char*>(p);
+      cap_host_ = bytes;
     }
     return host_;
   }
 
  private:
-  void grow_dev(std::size_t n) {
-    if (2 * n > cap_dev_) {
+  void grow_dev(std::size_t bytes, std::size_t work_bytes) {
+    bytes = (bytes + 255) / 256 * 256;
+    if (bytes > half_ || 2 * bytes + work_bytes > cap_dev_) {
       if (dev_) check(pl_device_free(dev_));
       dev_ = nullptr;
       void* p = nullptr;
-      check(pl_device_alloc(&p, 2 * n * sizeof(float)));
-      dev_ = static_cast<float*>(p);
-      cap_dev_ = 2 * n;
+      const std::size_t cap = 2 * bytes + work_bytes;
+      check(pl_device_alloc(&p, cap));
+      dev_ = static_cast<char*>(p);
+      cap_dev_ = cap;
     }
+    half_ = bytes;
   }
   void* stream_ = nullptr;
-  float* dev_ = nullptr;
-  float* host_ = nullptr;
-  std::size_t cap_dev_ = 0, cap_host_ = 0;
+  char* dev_ = nullptr;
+  char* host_ = nullptr;
+  std::size_t cap_dev_ = 0, cap_host_ = 0, half_ = 0;
 };
 
 Staging& staging() {
@@ -151,7 +165,7 @@ template <typename Launch>
 std::vector<double> run_device(const std::vector<double>& in, int threads, Launch&& launch) {
   const std::size_t n = in.size();
   Staging& st = staging();
-  float* h = st.host(n);
+  float* h = static_cast<float*>(st.host(n * sizeof(float)));
   std::vector<double> lo_t(64, std::numeric_limits<double>::infinity()),
       hi_t(64, -std::numeric_limits<double>::infinity());
   parallel_chunks(n, threads, [&](std::size_t a, std::size_t b, unsigned k) {
@@ -168,8 +182,8 @@ std::vector<double> run_device(const std::vector<double>& in, int threads, Launc
   const double lo = *std::min_element(lo_t.begin(), lo_t.end());
   const double hi = *std::max_element(hi_t.begin(), hi_t.end());
   void* s = st.stream();
-  float* src = st.dev_src(n);
-  float* dst = st.dev_dst(n);
+  float* src = static_cast<float*>(st.dev_src(n * sizeof(float)));
+  float* dst = static_cast<float*>(st.dev_dst());
   check(pl_copy_to_device_async(src, h, n * sizeof(float), s));
   check(launch(src, dst, s));
   check(pl_copy_to_host_async(h, dst, n * sizeof(float), s));
@@ -183,6 +197,36 @@ std::vector<double> run_device(const std::vector<double>& in, int threads, Launc
   });
   return out;
 }
+
+// The reference-precision route: the doubles go to the device as they are
+// (pinned staging copy, parallel), `launch(src, dst, work, stream)` runs the
+// fp64 kernels, and the results come back as doubles -- no conversion.
+template <typename Launch>
+std::vector<double> run_device64(const std::vector<double>& in, int threads, std::size_t work_bytes,
+                                 Launch&& launch) {
+  const std::size_t n = in.size(), bytes = n * sizeof(double);
+  Staging& st = staging();
+  double* h = static_cast<double*>(st.host(bytes));
+  parallel_chunks(n, threads, [&](std::size_t a, std::size_t b, unsigned) {
+    std::memcpy(h + a, in.data() + a, (b - a) * sizeof(double));
+  });
+  void* s = st.stream();
+  double* src = static_cast<double*>(st.dev_src(bytes, work_bytes));
+  double* dst = static_cast<double*>(st.dev_dst());
+  double* work = static_cast<double*>(st.dev_work());
+  check(pl_copy_to_device_async(src, h, bytes, s));
+  check(launch(src, dst, work, s));
+  check(pl_copy_to_host_async(h, dst, bytes, s));
+  check(pl_stream_synchronize(s));
+  std::vector<double> out(n);
+  parallel_chunks(n, threads, [&](std::size_t a, std::size_t b, unsigned) {
+    std::memcpy(out.data() + a, h + a, (b - a) * sizeof(double));
+  });
+  return out;
+}
+
+std::atomic<int> g_precision{static_cast<int>(DevicePrecision::reference_fp64)};
+bool fp64() { return g_precision.load(std::memory_order_relaxed) == static_cast<int>(DevicePrecision::reference_fp64); }
 
 pl_params to_pl(const NlmParams& p) { return pl_params{p.search_radius, p.patch_radius, p.h}; }
 
@@ -205,6 +249,24 @@ enum class Op { Row, Col, RowCol, ColRow, Snlm, Naive2d };
 Image2D run_image(const Image2D& img, const NlmParams& p, Op op, int threads) {
   const int R = img.rows, C = img.cols;
   const pl_params pp = to_pl(p);
+  if (fp64()) {
+    const int wop = op == Op::Snlm ? 2 : (op == Op::ColRow ? 1 : 0);
+    const std::size_t work = (op == Op::Row || op == Op::Col || op == Op::Naive2d)
+                                 ? 0 : 2 * pl_workspace_bytes(wop, 1, R, C);
+    std::vector<double> out =
+        run_device64(img.data, threads, work, [&](double* src, double* dst, double* w, void* s) {
+          switch (op) {
+            case Op::Row: return pl_nlm_row_pass_f64(src, dst, 1, R, C, pp, s);
+            case Op::Col: return pl_nlm_col_pass_f64(src, dst, 1, R, C, pp, s);
+            case Op::RowCol: return pl_snlm_2d_row_col_f64(src, dst, w, 1, R, C, pp, s);
+            case Op::ColRow: return pl_snlm_2d_col_row_f64(src, dst, w, 1, R, C, pp, s);
+            case Op::Snlm: return pl_snlm_2d_f64(src, dst, w, 1, R, C, pp, s);
+            case Op::Naive2d: return pl_nlm_2d_naive_f64(src, dst, 1, R, C, pp, s);
+          }
+          return static_cast<int>(PL_ERR_ARG);
+        });
+    return Image2D(R, C, std::move(out));
+  }
   std::vector<double> out = run_device(img.data, threads, [&](float* src, float* dst, void* s) {
     switch (op) {
       case Op::Row: return pl_nlm_row_pass(src, dst, 1, R, C, pp, s);
@@ -227,6 +289,10 @@ bool identity_cols(const Image2D& img, const NlmParams& p) {
 }
 
 }  // namespace
+
+// ---- device precision (b200.hpp, an extension of the reference API) ----------
+void set_device_precision(DevicePrecision p) { g_precision.store(static_cast<int>(p)); }
+DevicePrecision device_precision() { return static_cast<DevicePrecision>(g_precision.load()); }
 
 // ---- core types (core_types.cpp:20-98) --------------------------------------
 Signal1D::Signal1D(std::vector<double> values) : samples(std::move(values)) {
@@ -354,6 +420,10 @@ Signal1D nlm_1d_patchlift(const Signal1D& f, const NlmParams& p, OpCounter* ops)
   add_counts_1d(n, p, 1, ops);
   if (std::min(p.search_radius, n - 1) == 0) return f;
   const pl_params pp = to_pl(p);
+  if (fp64())
+    return Signal1D(run_device64(f.samples, 0, 0, [&](double* src, double* dst, double*, void* s) {
+      return pl_nlm_lines_f64(src, dst, 1, n, n, pp, s);
+    }));
   return Signal1D(run_device(f.samples, 0, [&](float* src, float* dst, void* s) {
     return pl_nlm_lines(src, dst, 1, n, n, pp, s);
   }));
@@ -374,6 +444,10 @@ Signal1D nlm_1d_naive(const Signal1D& f, const NlmParams& p, OpCounter* ops) {
   }
   if (std::min(p.search_radius, n - 1) == 0) return f;
   const pl_params pp = to_pl(p);
+  if (fp64())
+    return Signal1D(run_device64(f.samples, 0, 0, [&](double* src, double* dst, double*, void* s) {
+      return pl_nlm_lines_naive_f64(src, dst, 1, n, n, pp, s);
+    }));
   return Signal1D(run_device(f.samples, 0, [&](float* src, float* dst, void* s) {
     return pl_nlm_lines_naive(src, dst, 1, n, n, pp, s);
   }));

@@ -417,12 +417,13 @@ class Scratch {
   }
   Scratch(const Scratch&) = delete;
   Scratch& operator=(const Scratch&) = delete;
-  int alloc(size_t bytes, float** out) {
+  template <typename T>
+  int alloc(size_t bytes, T** out) {
     cudaMemPool_t pool;
     int rc = device_pool(&pool);
     if (rc) return rc;
     PL_CUDA(cudaMallocFromPoolAsync(&ptr_, bytes ? bytes : 16, pool, st_));
-    *out = static_cast<float*>(ptr_);
+    *out = static_cast<T*>(ptr_);
     return PL_OK;
   }
 
@@ -983,6 +984,170 @@ int pl_banded_kernel_f64(const double* src, double* band, int64_t n_lines, int32
 }  // extern "C"
 
 extern "C" {
+
+// ---- fp64 reference-precision route (plgpu_walk64.cuh) -----------------------
+}  // extern "C"
+
+namespace {
+
+plgpu::Pass64Desc desc64(const double* src, double* dst, int batch, int rows, int cols, bool col) {
+  plgpu::Pass64Desc g{};
+  g.src = src;
+  g.dst = dst;
+  g.n_lines = (int64_t)batch * (col ? cols : rows);
+  g.lines_per_img = col ? cols : rows;
+  g.src_img_stride = g.dst_img_stride = (int64_t)rows * cols;
+  g.src_line_stride = g.dst_line_stride = col ? 1 : cols;
+  g.src_pos_stride = g.dst_pos_stride = col ? cols : 1;
+  g.n = col ? rows : cols;
+  return g;
+}
+
+int run_pass64(plgpu::Pass64Desc g, const pl_params& p, cudaStream_t st) {
+  g.S = std::min<int32_t>(p.search_radius, g.n - 1);
+  g.K = p.patch_radius;
+  g.inv_h2 = 1.0 / (p.h * p.h);
+  g.seg_len = segment_length(g.n, g.S);
+  g.nseg = (g.n + g.seg_len - 1) / g.seg_len;
+  if (g.n_lines <= 0) return PL_OK;
+  if (g.S >= 1 && g.S <= kMaxWalkS) {
+    g_route = "f64<S=" + std::to_string(template_radius(g.S)) + ">";
+    switch (template_radius(g.S)) {
+#define PL_CASE(v) \
+  case v: plgpu::launch_pass64<v>(g, st); break;
+      PLGPU_FOR_EACH_RADIUS(PL_CASE)
+#undef PL_CASE
+    }
+    return check_launch();
+  }
+  g_route = "f64-direct";
+  const int64_t work = g.n_lines * g.n;
+  plgpu::direct_pass64_kernel<<<(unsigned)((work + 127) / 128), 128, 0, st>>>(g);
+  return check_launch();
+}
+
+int image_checks64(const double* src, const double* dst, int batch, int rows, int cols,
+                   const pl_params& p) {
+  int rc = validate_image(batch, rows, cols);
+  if (!rc) rc = validate_params(p, rows);
+  if (!rc) rc = validate_params(p, cols);
+  if (!rc) rc = check_ptrs(src, dst);
+  return rc;
+}
+
+}  // namespace
+
+extern "C" {
+
+int pl_nlm_lines_f64(const double* src, double* dst, int64_t n_lines, int32_t n, int64_t ld,
+                     pl_params p, void* stream) {
+  int rc = validate_params(p, n);
+  if (!rc) rc = check_ptrs(src, dst);
+  if (rc) return rc;
+  plgpu::Pass64Desc g{};
+  g.src = src;
+  g.dst = dst;
+  g.n_lines = n_lines;
+  g.lines_per_img = (int32_t)std::max<int64_t>(1, std::min<int64_t>(n_lines, INT32_MAX));
+  g.src_img_stride = g.dst_img_stride = ld * g.lines_per_img;
+  g.src_line_stride = g.dst_line_stride = ld;
+  g.src_pos_stride = g.dst_pos_stride = 1;
+  g.n = n;
+  return run_pass64(g, p, as_stream(stream));
+}
+
+int pl_nlm_lines_naive_f64(const double* src, double* dst, int64_t n_lines, int32_t n, int64_t ld,
+                           pl_params p, void* stream) {
+  int rc = validate_params(p, n);
+  if (!rc) rc = check_ptrs(src, dst);
+  if (rc) return rc;
+  if (n_lines <= 0) return PL_OK;
+  plgpu::Pass64Desc g{};
+  g.src = src;
+  g.dst = dst;
+  g.n_lines = n_lines;
+  g.lines_per_img = (int32_t)std::max<int64_t>(1, std::min<int64_t>(n_lines, INT32_MAX));
+  g.src_img_stride = g.dst_img_stride = ld * g.lines_per_img;
+  g.src_line_stride = g.dst_line_stride = ld;
+  g.src_pos_stride = g.dst_pos_stride = 1;
+  g.n = n;
+  g.S = p.search_radius;  // the naive route does not clip S (windows are clipped per pixel)
+  g.K = p.patch_radius;
+  g.inv_h2 = 1.0 / (p.h * p.h);
+  const int64_t work = n_lines * n;
+  plgpu::direct_pass64_kernel<<<(unsigned)((work + 127) / 128), 128, 0, as_stream(stream)>>>(g);
+  return check_launch();
+}
+
+int pl_nlm_row_pass_f64(const double* src, double* dst, int32_t batch, int32_t rows, int32_t cols,
+                        pl_params p, void* stream) {
+  int rc = validate_image(batch, rows, cols);
+  if (!rc) rc = validate_params(p, cols);
+  if (!rc) rc = check_ptrs(src, dst);
+  if (rc) return rc;
+  return run_pass64(desc64(src, dst, batch, rows, cols, false), p, as_stream(stream));
+}
+
+int pl_nlm_col_pass_f64(const double* src, double* dst, int32_t batch, int32_t rows, int32_t cols,
+                        pl_params p, void* stream) {
+  int rc = validate_image(batch, rows, cols);
+  if (!rc) rc = validate_params(p, rows);
+  if (!rc) rc = check_ptrs(src, dst);
+  if (rc) return rc;
+  return run_pass64(desc64(src, dst, batch, rows, cols, true), p, as_stream(stream));
+}
+
+int pl_snlm_2d_row_col_f64(const double* src, double* dst, double* work, int32_t batch,
+                           int32_t rows, int32_t cols, pl_params p, void* stream) {
+  int rc = image_checks64(src, dst, batch, rows, cols, p);
+  if (rc) return rc;
+  cudaStream_t st = as_stream(stream);
+  Scratch scratch(st);
+  if (!work && (rc = scratch.alloc(2 * pl_workspace_bytes(0, batch, rows, cols), &work))) return rc;
+  if ((rc = run_pass64(desc64(src, work, batch, rows, cols, false), p, st))) return rc;
+  return run_pass64(desc64(work, dst, batch, rows, cols, true), p, st);
+}
+
+int pl_snlm_2d_col_row_f64(const double* src, double* dst, double* work, int32_t batch,
+                           int32_t rows, int32_t cols, pl_params p, void* stream) {
+  int rc = image_checks64(src, dst, batch, rows, cols, p);
+  if (rc) return rc;
+  cudaStream_t st = as_stream(stream);
+  Scratch scratch(st);
+  if (!work && (rc = scratch.alloc(2 * pl_workspace_bytes(1, batch, rows, cols), &work))) return rc;
+  if ((rc = run_pass64(desc64(src, work, batch, rows, cols, true), p, st))) return rc;
+  return run_pass64(desc64(work, dst, batch, rows, cols, false), p, st);
+}
+
+int pl_snlm_2d_f64(const double* src, double* dst, double* work, int32_t batch, int32_t rows,
+                   int32_t cols, pl_params p, void* stream) {
+  int rc = image_checks64(src, dst, batch, rows, cols, p);
+  if (rc) return rc;
+  cudaStream_t st = as_stream(stream);
+  Scratch scratch(st);
+  if (!work && (rc = scratch.alloc(2 * pl_workspace_bytes(2, batch, rows, cols), &work))) return rc;
+  const int64_t cnt = (int64_t)batch * rows * cols;
+  double* cr_img = work;
+  double* mid = work + cnt;
+  if ((rc = pl_snlm_2d_col_row_f64(src, cr_img, mid, batch, rows, cols, p, stream))) return rc;
+  if ((rc = run_pass64(desc64(src, mid, batch, rows, cols, false), p, st))) return rc;
+  plgpu::Pass64Desc g = desc64(mid, dst, batch, rows, cols, true);
+  g.avg = cr_img;  // (CR + RC) / 2 fused into the final store (average(), nlm.cpp:106-112)
+  return run_pass64(g, p, st);
+}
+
+int pl_nlm_2d_naive_f64(const double* src, double* dst, int32_t batch, int32_t rows, int32_t cols,
+                        pl_params p, void* stream) {
+  int rc = validate_image(batch, rows, cols);
+  if (!rc) rc = validate_params(p, std::min(rows, cols));
+  if (!rc) rc = check_ptrs(src, dst);
+  if (rc) return rc;
+  plgpu::Naive2D64Desc g{src, dst, batch, rows, cols, p.search_radius, p.patch_radius,
+                         1.0 / (p.h * p.h)};
+  const int64_t work = (int64_t)batch * rows * cols;
+  plgpu::nlm_2d_naive64_kernel<<<(unsigned)((work + 127) / 128), 128, 0, as_stream(stream)>>>(g);
+  return check_launch();
+}
 
 int pl_nlm_2d_naive(const float* src, float* dst, int32_t batch, int32_t rows, int32_t cols,
                     pl_params p, void* stream) {

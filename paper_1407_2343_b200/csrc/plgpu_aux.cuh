@@ -10,6 +10,7 @@
 #include <cstdint>
 
 #include "plgpu_walk.cuh"
+#include "plgpu_walk64.cuh"
 
 namespace plgpu {
 
@@ -153,6 +154,85 @@ __global__ void __launch_bounds__(128) distance_band_direct_kernel(BandDesc g) {
     }
     band[j - i + g.S_band] = band_cast<T>(dsq);
   }
+}
+
+}  // namespace plgpu
+
+namespace plgpu {
+
+// Direct route in double (S = 0 or S above the walker range): every window
+// of pixel i summed from scratch, ascending j (nlm.cpp:66-81).
+__global__ void __launch_bounds__(128) direct_pass64_kernel(Pass64Desc g) {
+  const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= g.n_lines * g.n) return;
+  const int64_t line = w % g.n_lines;
+  const int i = (int)(w / g.n_lines);
+  const int64_t img = line / g.lines_per_img;
+  const int64_t li = line - img * g.lines_per_img;
+  const double* f = g.src + img * g.src_img_stride + li * g.src_line_stride;
+  const int64_t ps = g.src_pos_stride;
+  const int n = g.n, K = g.K;
+  const int lo = max(0, i - g.S), hi = min(n - 1, i + g.S);
+  double num = 0.0, den = 0.0, vmin = 1.7976931348623157e308, vmax = -vmin;
+  for (int j = lo; j <= hi; ++j) {
+    double dsq = 0.0;
+    for (int t = -K; t <= K; ++t) {
+      const double df = __ldg(f + mirror_pos(i + t, n) * ps) - __ldg(f + mirror_pos(j + t, n) * ps);
+      dsq = fma(df, df, dsq);
+    }
+    const double wt = (j == i) ? 1.0 : exp(-dsq * g.inv_h2);
+    const double fj = __ldg(f + (int64_t)j * ps);
+    num = fma(wt, fj, num);
+    den += wt;
+    vmin = fmin(vmin, fj);
+    vmax = fmax(vmax, fj);
+  }
+  double* dst = g.dst + img * g.dst_img_stride + li * g.dst_line_stride + (int64_t)i * g.dst_pos_stride;
+  double v = fmin(fmax(num / den, vmin), vmax);
+  if (g.avg) v = (g.avg[dst - g.dst] + v) / 2.0;
+  *dst = v;
+}
+
+}  // namespace plgpu
+
+namespace plgpu {
+
+struct Naive2D64Desc {
+  const double* src;
+  double* dst;
+  int32_t batch, rows, cols, S, K;
+  double inv_h2;
+};
+
+// Classical 2D NLM in double (nlm_2d_naive, nlm.cpp:168-213), the drop-in's
+// reference-precision baseline: clipped (2S+1)^2 window, (2K+1)^2 patches
+// over the per-axis half-sample mirror, exp(-d / (h h)).
+__global__ void __launch_bounds__(128) nlm_2d_naive64_kernel(Naive2D64Desc g) {
+  const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t plane = (int64_t)g.rows * g.cols;
+  if (w >= plane * g.batch) return;
+  const int64_t b = w / plane;
+  const int r = (int)((w % plane) / g.cols), c = (int)(w % g.cols);
+  const double* img = g.src + b * plane;
+  const int H = g.rows, W = g.cols, S = g.S, K = g.K;
+  auto px = [&](int y, int x) { return __ldg(img + (int64_t)mirror_pos(y, H) * W + mirror_pos(x, W)); };
+  double num = 0.0, den = 0.0, vmin = 1.7976931348623157e308, vmax = -vmin;
+  for (int r2 = max(0, r - S); r2 <= min(H - 1, r + S); ++r2)
+    for (int c2 = max(0, c - S); c2 <= min(W - 1, c + S); ++c2) {
+      double dsq = 0.0;
+      for (int py = -K; py <= K; ++py)
+        for (int qx = -K; qx <= K; ++qx) {
+          const double df = px(r + py, c + qx) - px(r2 + py, c2 + qx);
+          dsq = fma(df, df, dsq);
+        }
+      const double wt = (r2 == r && c2 == c) ? 1.0 : exp(-dsq * g.inv_h2);
+      const double v = __ldg(img + (int64_t)r2 * W + c2);
+      num = fma(wt, v, num);
+      den += wt;
+      vmin = fmin(vmin, v);
+      vmax = fmax(vmax, v);
+    }
+  g.dst[w] = fmin(fmax(num / den, vmin), vmax);
 }
 
 }  // namespace plgpu

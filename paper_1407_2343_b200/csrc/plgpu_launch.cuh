@@ -11,11 +11,14 @@
 #include "plgpu_walk.cuh"
 #include "plgpu_walk2.cuh"
 #include "plgpu_walk3.cuh"
+#include "plgpu_walk64.cuh"
 
 namespace plgpu {
 
 template <int ST>
 void launch_pass(const PassDesc& g, cudaStream_t st);
+
+// fp64 reference-precision walker (plgpu_walk64.cuh), defined inline there.
 
 template <int ST, typename T>
 void launch_band(const BandDesc& g, cudaStream_t st);
@@ -129,6 +132,7 @@ bool launch_pass3(const Pass3Desc& d, int io, cudaStream_t st) {
   template bool launch_pass3<ST>(const Pass3Desc&, int, cudaStream_t);     \
   template void launch_pass<ST>(const PassDesc&, cudaStream_t);            \
   template void launch_pass2<ST>(const Pass2Desc&, bool, cudaStream_t);    \
+  template void launch_pass64<ST>(const Pass64Desc&, cudaStream_t);        \
   template void launch_band<ST, float>(const BandDesc&, cudaStream_t);     \
   template void launch_band<ST, int32_t>(const BandDesc&, cudaStream_t);
 #endif

@@ -4,15 +4,17 @@
 // sec. 3 call shape).  Each call converts double -> fp32, copies to the B200,
 // runs both passes, copies back and widens to double.
 //
-//   dropin_bench <image.f32> <rows> <cols> <S> <K> <h> <calls> [threads]
+//   dropin_bench <image.f32> <rows> <cols> <S> <K> <h> <calls> [threads] [fp64|fp32]
 //
 // The image file holds rows*cols little-endian fp32 samples.  Prints one JSON
 // line: Mpixel/s over <calls> timed calls after one warm-up call.
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <string>
 #include <vector>
 
+#include "patchlift/b200.hpp"
 #include "patchlift/core_types.hpp"
 #include "patchlift/nlm.hpp"
 
@@ -25,6 +27,9 @@ int main(int argc, char** argv) {
   const patchlift::NlmParams p{std::atoi(argv[4]), std::atoi(argv[5]), std::atof(argv[6])};
   const int calls = std::atoi(argv[7]);
   const int threads = argc > 8 ? std::atoi(argv[8]) : 0;
+  const bool fp32 = argc > 9 && std::string(argv[9]) == "fp32";
+  patchlift::set_device_precision(fp32 ? patchlift::DevicePrecision::fast_fp32
+                                        : patchlift::DevicePrecision::reference_fp64);
   std::vector<float> raw(static_cast<std::size_t>(rows) * cols);
   FILE* f = std::fopen(argv[1], "rb");
   if (!f || std::fread(raw.data(), sizeof(float), raw.size(), f) != raw.size()) {
@@ -40,7 +45,8 @@ int main(int argc, char** argv) {
   double sum = 0.0;
   for (double v : out.data) sum += v;
   std::printf("{\"mpx_s\": %.6g, \"s_per_call\": %.6g, \"calls\": %d, \"threads\": %d, "
-              "\"checksum\": %.17g}\n",
-              static_cast<double>(rows) * cols * calls / s / 1e6, s / calls, calls, threads, sum);
+              "\"precision\": \"%s\", \"checksum\": %.17g}\n",
+              static_cast<double>(rows) * cols * calls / s / 1e6, s / calls, calls, threads,
+              fp32 ? "fp32" : "fp64", sum);
   return 0;
 }

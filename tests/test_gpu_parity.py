@@ -670,3 +670,30 @@ def test_guard_bands_no_stray_access():
             pl.nlm_1d_patchlift(line.contiguous(), p, out=out1)
             torch.cuda.synchronize()
             assert torch.isfinite(out1).all() and (dst[:G] == -7.0).all()
+
+
+def test_f64_route_matches_reference_library(ref):
+    """The fp64 route (plgpu_walk64.cuh; the C++ drop-in's default) against the
+    UNMODIFIED reference library on the same double inputs: every filter
+    within 1e-9 on [0, 255] data (the reference's own filter-equivalence
+    tolerance, acceptance_main.cpp:87-122), including edges, S > 32 (direct
+    route) and S = 0."""
+    rng = np.random.default_rng(64)
+    for (r, c, S, K, h) in [(40, 57, 5, 2, 30.0), (33, 70, 10, 3, 74.8), (64, 48, 16, 5, 15.0),
+                            (20, 90, 25, 7, 136.9), (12, 100, 40, 1, 50.0), (9, 30, 0, 2, 20.0),
+                            (50, 50, 7, 0, 8.0)]:
+        img = rng.uniform(0, 255, (r, c))
+        x = torch.from_numpy(img).cuda()
+        for op in ("row", "col", "rc", "cr", "snlm", "nlm2d"):
+            got = pl.filter_f64(op, x, (S, K, h)).cpu().numpy()
+            want = ref.filter(op if op != "nlm2d" else "nlm2d", img, S, K, h)
+            err = float(np.abs(got - want).max())
+            assert err <= 1e-9, (op, r, c, S, K, h, err)
+    for (n, S, K, h) in [(300, 10, 3, 60.0), (77, 5, 8, 15.0), (1000, 32, 7, 200.0)]:
+        f = rng.uniform(0, 255, (3, n))
+        x = torch.from_numpy(f).cuda()
+        for op, naive in (("lines", False), ("lines_naive", True)):
+            got = pl.filter_f64(op, x, (S, K, h)).cpu().numpy()
+            for row in range(3):
+                want = ref.nlm_1d(f[row], S, K, h, naive=naive)
+                assert float(np.abs(got[row] - want).max()) <= 1e-9, (op, n, S, K)
