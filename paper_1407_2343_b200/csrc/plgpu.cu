@@ -255,6 +255,10 @@ int try_pass2(const plgpu::PassDesc& g, cudaStream_t st) {
                          g.src_img_stride % 4 == 0 && a16(g.src);
       // io 0: 16-byte staging copies and stores; io 2: 16-byte stores only
       d3.b.vec16 = io == 0 ? (dst16 && src16) : io == 2 ? dst16 : false;
+      // The 2-line column flush stores from registers at base + q * pitch:
+      // it needs the aligned layout and a 32-bit R * pitch; walk2 otherwise.
+      const bool own_ok = d3.b.vec16 && (uint64_t)g.dst_pos_stride * sizeof(float) * R < (1ull << 32);
+      if (d3.lines == 2 && io != 1 && !own_ok) goto staged;
       int lo = d.nseg, hi = -1;
       for (int sgi = 0; sgi < d.nseg; ++sgi) {
         const int s0 = (d.seg_begin + sgi) * d.seg_len, s1 = std::min(d.n, s0 + d.seg_len);
@@ -290,6 +294,7 @@ int try_pass2(const plgpu::PassDesc& g, cudaStream_t st) {
       }
     }
   }
+staged:
   g_route = "staged<S=" + std::to_string(ST) + ",rows=" + std::to_string(rows ? 1 : 0) + ">";
   if (g.dexp) return set_err(PL_ERR_UNSUPPORTED, "distance export needs the hot kernel's (K, S)");
   switch (ST) {

@@ -87,6 +87,19 @@ __host__ __device__ constexpr bool pass3_split(int ST) { return ST > 16; }  // S
 // walk computes for a pixel of this segment is also stored into g.dexp, so
 // the exactness of the code that actually runs can be checked (with the
 // prescale set to 1 the recurrence runs on the raw samples).
+// base + q * stride as one 32x32 -> 64-bit multiply-add (IMAD.WIDE.U32; with q
+// a compile-time constant after unrolling ptxas takes it as an immediate).
+template <typename T>
+__device__ __forceinline__ T* mad_wide_u32(uint32_t q, uint32_t stride, T* base) {
+  T* r;
+  asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(r) : "r"(q), "r"(stride), "l"(base));
+  return r;
+}
+
+__device__ __forceinline__ void st_global_f2(void* p, float2 v) {
+  asm volatile("st.global.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(v.x), "f"(v.y) : "memory");
+}
+
 template <int ST, int KT, int LINES, int IO, int MODE = 0, bool AVG = false, bool EXP = false>
 __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int lane,
                                       const int64_t grp, const int seg, const int bar_threads = 0) {
@@ -123,9 +136,13 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
   for (int x = 0; x < g.nx; ++x) fan |= l0 < g.xhi[x] && l0 + LW > g.xlo[x];
   // Column pass with 2 lines per lane: every lane stages (8-byte copies) and
   // flushes exactly the lines it computes -> no warp barriers around the ring.
-  const bool own = !ROWS && LINES == 2 && g.vec16;
+  // (the host routes 2-line column-flush passes here only when they are
+  // 16-byte aligned with whole line groups, g.vec16; otherwise to walk2)
+  constexpr bool own = !ROWS && LINES == 2;
   // column-mode flush where each lane stores exactly the lines it computed
-  const bool oown = !OROWS && LINES == 2 && g.vec16;
+  // 2-line column flush: each lane stores its own two lines from registers
+  // (no output ring, no warp barrier)
+  constexpr bool oown = !OROWS && LINES == 2;
 
   auto slot = [&](int c) -> float* { return ring + (c & (kNS3 - 1)) * CHUNK; };
   // Copy chunk c (positions u = cR + BASE + q, q < R); always commits a group.
@@ -341,6 +358,7 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
     // leaves the line (the common case, branch-free); MASK = true: the last,
     // partial or clipped iteration(s) -- per-step exit, pairs beyond the line
     // end (or k > S) get weight exactly 0.
+    float2 outv[oown ? R : 1];  // this iteration's outputs (2-line column flush)
     auto body = [&](auto mask_tag) {
       constexpr bool MASK = decltype(mask_tag)::value;
       V xprev;  // x of the previous (even) step, tracked with the next
@@ -406,7 +424,9 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
         const float o0 = fminf(fmaxf(Ops::lo(qv), lo0), hi0);
         float o1 = o0;
         if constexpr (LINES == 2) o1 = fminf(fmaxf(Ops::hi(qv), lo1), hi1);
-        {  // every step lands in the output ring, filtered at the flush
+        if constexpr (oown) {
+          outv[r] = make_float2(o0, o1);
+        } else {  // every step lands in the output ring, filtered at the flush
           float* sl = oring + r * OPITCH + lane * LINES;
           if constexpr (LINES == 2) *reinterpret_cast<float2*>(sl) = make_float2(o0, o1);
           else *sl = o0;
@@ -420,8 +440,8 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
         else if constexpr (PK) frp[r] = f2_make(Ops::lo(fnew), 1.f);
         else fr[r] = fnew;
         // The leaving-term partner entering now (coordinate s+1+ST) entered
-        // the nr ring 2K+1 steps ago and is still there when 2K < S.
-        // The leaving partner entering now is copied from the nr ring (2-line
+        // the nr ring 2K+1 steps ago and is still there when 2K < S: it is
+        // copied from the nr ring (2-line
         // kernel) or re-read from the staged chunk and scaled (1-line kernels:
         // the copy's register shuffles cost c3 2.5 %; S = 25 spills with it).
         if constexpr (2 * KT < ST && ST <= 16 && LINES == 2) orr[r] = nr[(r + R - 2 * KT - 1) % R];
@@ -444,43 +464,39 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
 
     if constexpr (!OROWS) {
       // flush this iteration's outputs (row q = position i0 + sb + q)
-      if (oown) {  // each lane stores its own lines: no warp barrier
-        float* dp = g.dst + dst_img + (int64_t)(i0 + sb) * g.dst_pos_stride + my_line;
-        const float* sp = oring + LINES * lane;
+      if constexpr (oown) {  // each lane stores its own two lines, from registers
+        // position q's address = base + q * pitch (one IMAD.WIDE with the
+        // immediate q; the host keeps R * pitch < 2^32)
+        const uint32_t pitch = (uint32_t)g.dst_pos_stride * (uint32_t)sizeof(float);
+        char* const base = reinterpret_cast<char*>(g.dst + dst_img + (int64_t)(i0 + sb) * g.dst_pos_stride +
+                                                   my_line);
+        const bool whole = i0 + sb >= s0 && i0 + sb + R <= s1;
         if constexpr (AVG) {  // fused S-NLM average: all partner loads before any store
-          const float2* ap = reinterpret_cast<const float2*>(g.avg + (dp - g.dst));
-          const bool whole = i0 + sb >= s0 && i0 + sb + R <= s1;
+          const char* const abase = reinterpret_cast<const char*>(g.avg) +
+                                    (base - reinterpret_cast<char*>(g.dst));
           float2 a[R];
 #pragma unroll
           for (int q = 0; q < R; ++q) {
             const int p = i0 + sb + q;
-            a[q] = (whole || (p >= s0 && p < s1)) ? __ldg(ap) : make_float2(0.f, 0.f);
-            ap += g.dst_pos_stride / 2;
+            a[q] = (whole || (p >= s0 && p < s1))
+                       ? __ldg(reinterpret_cast<const float2*>(mad_wide_u32(q, pitch, abase)))
+                       : make_float2(0.f, 0.f);
           }
 #pragma unroll
           for (int q = 0; q < R; ++q) {
             const int p = i0 + sb + q;
-            if (whole || (p >= s0 && p < s1)) {
-              const float2 v = *reinterpret_cast<const float2*>(sp);
-              *reinterpret_cast<float2*>(dp) = make_float2((a[q].x + v.x) / 2.0f, (a[q].y + v.y) / 2.0f);
-            }
-            dp += g.dst_pos_stride;
-            sp += OPITCH;
+            if (whole || (p >= s0 && p < s1))
+              st_global_f2(mad_wide_u32(q, pitch, base),
+                           make_float2((a[q].x + outv[q].x) / 2.0f, (a[q].y + outv[q].y) / 2.0f));
           }
-        } else if (i0 + sb >= s0 && i0 + sb + R <= s1) {  // whole iteration inside [s0, s1)
+        } else if (whole) {
 #pragma unroll
-          for (int q = 0; q < R; ++q) {
-            *reinterpret_cast<float2*>(dp) = *reinterpret_cast<const float2*>(sp);
-            dp += g.dst_pos_stride;
-            sp += OPITCH;
-          }
+          for (int q = 0; q < R; ++q) st_global_f2(mad_wide_u32(q, pitch, base), outv[q]);
         } else {
 #pragma unroll
           for (int q = 0; q < R; ++q) {
             const int p = i0 + sb + q;
-            if (p >= s0 && p < s1) *reinterpret_cast<float2*>(dp) = *reinterpret_cast<const float2*>(sp);
-            dp += g.dst_pos_stride;
-            sp += OPITCH;
+            if (p >= s0 && p < s1) st_global_f2(mad_wide_u32(q, pitch, base), outv[q]);
           }
         }
       } else if (g.vec16) {
