@@ -200,3 +200,30 @@ def test_rc_graph_replay_bitwise():
         want = pl.snlm_2d_row_col(x, p)
         torch.cuda.synchronize()
         assert torch.equal(y, want), t
+
+
+@pytest.mark.slow
+def test_bench_multi_rank_logic_gloo(tmp_path):
+    """bench.py's N > 1 path (c4 sharded strong + weak, the three c5 forms with
+    the bitwise check against the single-GPU RC) with 2 ranks over gloo, both
+    on cuda:0: a functional check of the multi-rank logic (timings meaningless,
+    the line says so); the fused form needs symmetric memory, which gloo lacks."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29533", os.path.join(root, "bench.py"),
+           "--gpus", "2", "--steps", "2", "--warmup", "1", "--dist-backend", "gloo",
+           "--e2e-steps", "1"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=1200, cwd=root)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads([x for x in r.stdout.splitlines() if x.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["scaling"] == "strong"
+    assert line["config"]["global_batch"] == 64 and line["e2e"]["matches_device_result"]
+    assert line["weak"]["images_per_rank"] == 64
+    forms = line["c5_forms"]
+    assert forms["slab"]["bitwise_equal_single_gpu_rc"] is True
+    assert forms["halo"]["bitwise_equal_single_gpu_rc"] is True
+    assert "unavailable" in forms["fused"]
