@@ -697,3 +697,20 @@ def test_f64_route_matches_reference_library(ref):
             for row in range(3):
                 want = ref.nlm_1d(f[row], S, K, h, naive=naive)
                 assert float(np.abs(got[row] - want).max()) <= 1e-9, (op, n, S, K)
+
+
+def test_small_h_f64_route_strict(ref):
+    """Small h (5..25 on 8-bit data), where the fp32 running sums lose
+    accuracy (test_small_h_conditioning): the fp64 route holds the reference
+    to 1e-9 -- far inside T2 -- for single passes and composites alike."""
+    rng = np.random.default_rng(55)
+    for t in range(8):
+        r, c = int(rng.integers(20, 120)), int(rng.integers(20, 120))
+        S, K = int(rng.integers(2, 26)), int(rng.integers(0, 4))
+        h = float(rng.uniform(5.0, 25.0))
+        img = rng.uniform(0, 255, (r, c))
+        x = torch.from_numpy(img).cuda()
+        for op in ("row", "col", "rc", "cr", "snlm"):
+            got = pl.filter_f64(op, x, (S, K, h)).cpu().numpy()
+            want = ref.filter(op, img, S, K, h)
+            assert float(np.abs(got - want).max()) <= 1e-9, (op, r, c, S, K, h)
