@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c4", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--no-graph", action="store_true",
+                    help="c1/c2: time eager launches instead of one CUDA graph of the K steps")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -389,6 +391,52 @@ def torch_empty_like_cpu(t):
 def torch_cat(parts):
     import torch
     return torch.cat(parts, 0)
+
+
+def timed_graph(D, first_pass, second_pass, steps, warmup):
+    """Launch-bound configs (c1: one ~10 us kernel per step; c2: two): the K
+    timed steps are captured into ONE CUDA graph and replayed with a single
+    launch, so the events bracket device time and not the Python/ctypes launch
+    path.  Per-pass times come from two more graphs (K first passes, K second
+    passes).  The eager per-step time is reported beside it."""
+    import torch
+
+    def capture(fns):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for _ in range(steps):
+                for fn in fns:
+                    fn()
+        return g
+
+    def replay_ms(g):
+        s = torch.cuda.current_stream()
+        for _ in range(max(3, warmup) // steps + 2):
+            g.replay()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        D.barrier()
+        torch.cuda.synchronize()
+        a.record(s)
+        g.replay()
+        b.record(s)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / steps
+
+    eager = timed(D, first_pass, second_pass, steps, warmup, clocks=False)
+    g_all, g_row, g_col = capture([first_pass, second_pass]), capture([first_pass]), capture([second_pass])
+    sampler = ClockSampler(D.dev.index)
+    sampler.__enter__()
+    try:
+        ms_step = D.max(replay_ms(g_all))
+        row_ms, col_ms = replay_ms(g_row), replay_ms(g_col)
+        if len(sampler.lines) < 3:
+            time.sleep(0.35)
+    finally:
+        sampler.__exit__(None, None, None)
+    return {"ms_step": ms_step, "row_ms": row_ms, "col_ms": col_ms, "clocks": sampler.summary(),
+            "eager_ms_step": eager["ms_step"],
+            "launch": f"CUDA graph: the {steps} timed steps captured once, one launch"}
 
 
 def timed(D, first_pass, second_pass, steps, warmup, clocks=True):
@@ -756,7 +804,10 @@ def run_ours(args):
             from paper_1407_2343_b200.distributed import shard
             lo, hi = shard(n_items, world, rank)
         run = BatchRun(D, pl, args.config, lo, hi, params)
-        t = timed(D, run.first_pass, run.second_pass, args.steps, args.warmup)
+        if args.config in ("c1", "c2") and world == 1 and not args.no_graph:
+            t = timed_graph(D, run.first_pass, run.second_pass, args.steps, args.warmup)
+        else:
+            t = timed(D, run.first_pass, run.second_pass, args.steps, args.warmup)
         px_total = c["n"] if run.signal else n_items * c["rows"] * c["cols"]
         roof = roofline(D, run.u_row, run.u_col, t, run.px_local, args.config, sms, f_max, live_peaks)
         e2e_s, bi, bo, ok = run.e2e(D, args.e2e_steps)
@@ -799,6 +850,9 @@ def run_ours(args):
         if D.backend != "nccl":
             line["functional_check_only"] = "gloo backend, all ranks on cuda:0: timings meaningless"
         line.update(extra)
+        if "launch" in t:
+            line["launch"] = t["launch"]
+            line["eager_ms_per_step"] = t["eager_ms_step"]
         if world == 1 and not c5_main and not run.signal:
             line["e2e_dropin"] = dropin_e2e(run.imgs_host[0], S, K, h, args.e2e_steps)
         if world == 1 and not args.no_cpu_baseline:

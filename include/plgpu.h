@@ -86,11 +86,30 @@ const char* pl_last_error(void);
  * "portable<...>", "direct", "none"); for composites, their last pass. */
 const char* pl_last_route(void);
 /* Debug / test hook: pin the kernel route process-wide.  walker 0 = default,
- * 1 = portable walker only, 2 = no hot-configuration kernel; lines 0/1/2 and
+ * 1 = portable walker only, 2 = no hot-configuration kernel, 3 = default
+ * walkers but few-line 1D calls are not folded onto lanes; lines 0/1/2 and
  * wpc 0/2/8 pin the hot kernel's lines per lane and warps per CTA (0 =
  * default).  Every route computes the same bits; this only selects code for
  * coverage and A/B timing.  (0, 0, 0) restores the defaults. */
 int pl_debug_set_route(int32_t walker, int32_t lines, int32_t wpc);
+/* Precision policy of the reference-API entry points (pl_nlm_lines,
+ * pl_nlm_row_pass, pl_nlm_col_pass, pl_snlm_2d_row_col, pl_snlm_2d_col_row,
+ * pl_snlm_2d, pl_snlm_2d_row_col_host).  The fp32 kernels hold the output
+ * bound (max abs error 1e-3 on a [0, 255] scale against the reference's
+ * double arithmetic) while h >= pl_fast_h_threshold() / 255 of the data range
+ * (40: every setting of the configs).  PL_PRECISION_AUTO
+ * (default): calls with h >= the threshold run the fp32 kernels directly;
+ * below it the input's range is measured (one reduction, the call then
+ * synchronises `stream`) and, if h is under threshold/255 of it, the call runs
+ * in double on the device (fp32 in, fp64 arithmetic and intermediates, fp32
+ * out: plgpu_walk64.cuh), slower but within the bound at any h.
+ * PL_PRECISION_FAST: always the fp32 kernels.  Process-wide.  The partition-
+ * level entry points (strided / blocked / window / fan-out passes, graphs)
+ * are fp32 only. */
+enum pl_precision_policy { PL_PRECISION_AUTO = 0, PL_PRECISION_FAST = 1 };
+int pl_set_precision_policy(int32_t policy);
+int32_t pl_precision_policy(void);
+double pl_fast_h_threshold(void);
 /* Name of the device the library will launch on, or "" if none. */
 const char* pl_device_name(void);
 

@@ -42,8 +42,9 @@ EXPORTS = [
     "pl_copy_to_host_async", "pl_debug_set_route", "pl_graph_rc_create", "pl_graph_launch",
     "pl_graph_destroy", "pl_nlm_lines_f64", "pl_nlm_lines_naive_f64", "pl_nlm_row_pass_f64",
     "pl_nlm_col_pass_f64", "pl_snlm_2d_row_col_f64", "pl_snlm_2d_col_row_f64", "pl_snlm_2d_f64",
-    "pl_nlm_2d_naive_f64",
+    "pl_nlm_2d_naive_f64", "pl_set_precision_policy", "pl_precision_policy", "pl_fast_h_threshold",
 ]
+PL_PRECISION_AUTO, PL_PRECISION_FAST = 0, 1
 PL_MAX_FANOUT = 2
 
 
@@ -93,6 +94,9 @@ def lib() -> C.CDLL:
             "pl_last_error": ([], C.c_char_p),
             "pl_last_route": ([], C.c_char_p),
             "pl_debug_set_route": ([i32, i32, i32], C.c_int),
+            "pl_set_precision_policy": ([i32], C.c_int),
+            "pl_precision_policy": ([], i32),
+            "pl_fast_h_threshold": ([], C.c_double),
             "pl_graph_rc_create": ([vp, vp, vp, i32, i32, i32, P, C.POINTER(vp)], C.c_int),
             "pl_graph_launch": ([vp, vp], C.c_int),
             "pl_graph_destroy": ([vp], C.c_int),
@@ -208,6 +212,29 @@ class debug_route:
 
     def __exit__(self, *a):
         lib().pl_debug_set_route(0, 0, 0)
+
+
+class precision_policy:
+    """Context manager for ``pl_set_precision_policy``: ``"auto"`` (default:
+    calls whose h is below ``fast_h_threshold()``/255 of the data range run in
+    double on the device) or ``"fast"`` (always the fp32 kernels)."""
+
+    def __init__(self, policy: str):
+        self.policy = {"auto": PL_PRECISION_AUTO, "fast": PL_PRECISION_FAST}[policy]
+
+    def __enter__(self):
+        self.prev = lib().pl_precision_policy()
+        _check(lib().pl_set_precision_policy(self.policy))
+        return self
+
+    def __exit__(self, *a):
+        _check(lib().pl_set_precision_policy(self.prev))
+        return False
+
+
+def fast_h_threshold() -> float:
+    """h (per 255 of data range) from which the fp32 kernels are used unconditionally."""
+    return float(lib().pl_fast_h_threshold())
 
 
 def last_route() -> str:

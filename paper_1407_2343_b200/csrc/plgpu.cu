@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <atomic>
+#include <limits>
 #include <mutex>
 #include <string>
 
@@ -79,13 +80,19 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 // line) 195 -> ~1,000 Msample/s on the B200 for S/64 extra pre-walk.  Short
 // lines (<= 1024 samples: small images, a few hundred lines each) also use
 // ~64-sample segments, so a 512^2 image runs 64 warps instead of 16.
+#ifndef PLGPU_SEG_MID
+#define PLGPU_SEG_MID 480
+#endif
+#ifndef PLGPU_SEG_LONG
+#define PLGPU_SEG_LONG 32
+#endif
 int32_t segment_length(int32_t n, int32_t S) {
   const int32_t R = std::max(1, S + 1);
   // long segments: pre-walk overhead S/C stays small
   // ~512 for lines up to 2048 samples: 4 segments of a 2048-sample line
   // instead of 5 (c4 +1.75 %; the per-GPU share of c4 at 8 GPUs, 8 images,
   // fits one wave: +18 %)
-  const int32_t target = (n >= 32768 || n <= 1024) ? 64 : (n <= 2048 ? 512 : 480);
+  const int32_t target = n >= 32768 ? PLGPU_SEG_LONG : n <= 1024 ? 64 : (n <= 2048 ? 512 : PLGPU_SEG_MID);
   int32_t nseg = std::max(1, (n + target - 1) / target);
   if (n >= 8192) nseg = std::max(8, (nseg + 4) / 8 * 8);
   int32_t C = (n + nseg - 1) / nseg;       // near-equal segments
@@ -104,6 +111,7 @@ int32_t segment_length(int32_t n, int32_t S) {
 std::atomic<int> g_dbg_walker{0};  // 0 default, 1 portable only, 2 no hot kernel
 std::atomic<int> g_dbg_lines{0};   // 0 default, 1 or 2 lines per lane (S <= 16)
 std::atomic<int> g_dbg_wpc{0};     // 0 default, 2 or 8 warps per CTA
+std::atomic<int> g_dbg_fold{0};    // 0 default, 2 = never fold 1D lines onto lanes
 
 bool force_portable() { return g_dbg_walker.load(std::memory_order_relaxed) == 1; }
 bool force_portable_v2() { return g_dbg_walker.load(std::memory_order_relaxed) == 2; }
@@ -117,8 +125,9 @@ int walk3_lines(int ST) {
 }
 int walk3_wpc(int ST) {
   const int forced = g_dbg_wpc.load(std::memory_order_relaxed);
-  if (forced == 2 || forced == 8) return forced;
-  return ST >= 15 ? 8 : 2;  // measured: lockstep helps S=15/25 (I-cache), hurts S=10
+  if (forced == 2) return 2;
+  if (forced == 8) return plgpu::kLockWpc;
+  return ST >= 15 ? plgpu::kLockWpc : 2;  // measured: lockstep helps S=15/25 (I-cache), hurts S=10
 }
 
 // Largest radius with a specialised walker; larger radii use the direct kernel.
@@ -187,8 +196,13 @@ int try_pass2(const plgpu::PassDesc& g, cudaStream_t st) {
   if (g.avg && g.dst_pos_stride == 1) return -1;  // fused average: column-mode flushes only
   // A warp carries 32-64 lines: for a handful of lines the one-thread-per-
   // segment portable walker wastes less.
-  if (force_portable() || g.K > 7 || g.S < 1 || g.S > kMaxWalkS || g.lines_per_img < 16) return -1;
+  // (unless the hot kernel can fold the lines' segments onto its lanes, below)
+  if (force_portable() || g.K > 7 || g.S < 1 || g.S > kMaxWalkS) return -1;
   const int ST = template_radius(g.S);
+  const bool few_lines = g.lines_per_img < 16;
+  if (few_lines && (force_portable_v2() || plgpu::pass3_k_for(ST) != g.K || ST != g.S ||
+                    g.src_pos_stride != 1 || g.dst_pos_stride != 1))
+    return -1;
   // fan-out stores: hot kernel's row flush or the portable walker
   if (g.nx > 0 && (force_portable_v2() || plgpu::pass3_k_for(ST) != g.K || ST != g.S ||
                    g.src_pos_stride != 1 || g.dst_pos_stride != 1))
@@ -247,6 +261,12 @@ int try_pass2(const plgpu::PassDesc& g, cudaStream_t st) {
       d3.b = d;
       // lines per lane for the hot kernel (PLGPU_LINES=1|2 overrides)
       d3.lines = walk3_lines(ST);
+      // Small calls (c2: one 512^2 image = 64 two-line warps on 148 SMs) are
+      // latency-bound: one line per lane doubles the warps and shortens each
+      // warp's step (c2 +17 %); routing only, same bits.
+      if (d3.lines == 2 && g_dbg_lines.load(std::memory_order_relaxed) == 0 &&
+          images * ((g.lines_per_img + 63) / 64) * d.nseg < 148 * 4)
+        d3.lines = 1;
       d3.wpc = walk3_wpc(ST);
       const int LW3 = 32 * d3.lines;
       d3.b.groups_per_img = (g.lines_per_img + LW3 - 1) / LW3;
@@ -262,6 +282,63 @@ int try_pass2(const plgpu::PassDesc& g, cudaStream_t st) {
       // it needs the aligned layout and a 32-bit R * pitch; walk2 otherwise.
       const bool own_ok = d3.b.vec16 && (uint64_t)g.dst_pos_stride * sizeof(float) * R < (1ull << 32);
       if (d3.lines == 2 && io != 1 && !own_ok) goto staged;
+      // Few long lines (1D signals): fold the interior segments onto the
+      // lanes (plgpu_walk3.cuh, Pass3FoldDesc).  Whole lines only, plain
+      // row layout, contiguous line stack, segments long enough that an
+      // interior segment's halo stays inside its neighbours.
+      if (io == 1 && g_dbg_fold.load(std::memory_order_relaxed) != 2 && d.seg_begin == 0 &&
+          d.nseg == (d.n + d.seg_len - 1) / d.seg_len && d.nx == 0 && !d.avg && !d.dexp &&
+          d.dst_pos_block == d.n && g.lines_per_img < 32 &&
+          (images == 1 || (g.src_img_stride == g.src_line_stride * g.lines_per_img &&
+                           g.dst_img_stride == g.dst_line_stride * g.lines_per_img))) {
+        const int C = d.seg_len;
+        // interior segments j: j C - S - K - 1 >= 0 and (j + 1) C + S + K <= n - 1
+        const int jlo = 1;
+        const int jhi = (int)std::min<int64_t>(d.nseg - 1, ((int64_t)d.n - 1 - ST - KT3) / C - 1);
+        const int NL = jhi - jlo + 1;
+        if (C >= ST + KT3 + 1 && (C + ST) % R == 0 && NL >= 8) {
+          plgpu::Pass3FoldDesc f{};
+          const int64_t real_lines = g.n_lines;
+          // one line per lane unless that would exceed one wave of warps
+          const int fl = (ST <= 16 && real_lines * ((NL + 31) / 32) > 148 * 8) ? 2 : 1;
+          const int FLW = 32 * fl;
+          f.edge = d;
+          f.edge.groups_per_img = (g.lines_per_img + FLW - 1) / FLW;
+          f.edge.vec16 = 0;
+          f.jlo = jlo;
+          f.jhi = jhi;
+          f.edge_warps = images * f.edge.groups_per_img * (d.nseg - NL);
+          f.edge.total_warps = f.edge_warps;
+          f.fold = d;
+          f.fold.src = g.src + (int64_t)(jlo - 1) * C;
+          f.fold.dst = g.dst + (int64_t)(jlo - 1) * C;
+          f.fold.src_img_stride = g.src_line_stride;  // one virtual image per real line
+          f.fold.dst_img_stride = g.dst_line_stride;
+          f.fold.src_line_stride = f.fold.dst_line_stride = C;
+          f.fold.lines_per_img = NL;
+          f.fold.groups_per_img = (NL + FLW - 1) / FLW;
+          f.fold.n = 3 * C;
+          f.fold.dst_pos_block = 3 * C;
+          f.fold.seg_begin = 1;
+          f.fold.nseg = 1;
+          f.fold.vec16 = 0;
+          f.fold.total_warps = real_lines * f.fold.groups_per_img;
+          f.fold_ctas = (int32_t)((f.fold.total_warps + plgpu::kWarpsPerCta - 1) / plgpu::kWarpsPerCta);
+          bool launched = false;
+          switch (ST) {
+#define PL_CASE(v) \
+  case v: launched = plgpu::launch_pass3_fold<v>(f, fl, st); break;
+            PLGPU_FOR_EACH_RADIUS(PL_CASE)
+#undef PL_CASE
+          }
+          if (launched) {
+            g_route = "hot-fold<S=" + std::to_string(ST) + ",K=" + std::to_string(KT3) +
+                      ",lines=" + std::to_string(fl) + ",folded=" + std::to_string(NL) + ">";
+            return check_launch();
+          }
+        }
+      }
+      if (few_lines) return -1;  // not foldable: portable walker
       int lo = d.nseg, hi = -1;
       for (int sgi = 0; sgi < d.nseg; ++sgi) {
         const int s0 = (d.seg_begin + sgi) * d.seg_len, s1 = std::min(d.n, s0 + d.seg_len);
@@ -445,6 +522,85 @@ int check_ptrs(const void* a, const void* b) {
   return PL_OK;
 }
 
+// ---- precision policy --------------------------------------------------------
+// The fp32 walkers hold the 1e-3 output bound (on a [0, 255] scale) while
+// h >= ~0.16 x the data range (below that the moving sums
+// carry rounding of ulp(d / h^2) and a composite's second pass amplifies the
+// fp32 intermediate's quantisation by ~ 2 |df| |f - out| / h^2).  Under
+// PL_PRECISION_AUTO (default) the reference-API entry points therefore run
+// such calls in double on the device (plgpu_walk64.cuh: fp32 in, fp64
+// arithmetic and intermediates, fp32 out).  h >= 40 -- every 8-bit-scale
+// setting the fp32 kernels are bounded for -- goes straight to the fp32
+// kernels; below that the input's range is measured first (one reduction and a
+// stream synchronisation) and h is compared with 40/255 of it.
+std::atomic<int> g_policy{PL_PRECISION_AUTO};
+constexpr double kFastH = 40.0;  // per 255 of data range
+
+int choose_precise(const float* src, int64_t lines, int32_t n, int64_t ld, double h,
+                   cudaStream_t st, bool* precise) {
+  *precise = false;
+  if (g_policy.load(std::memory_order_relaxed) == PL_PRECISION_FAST || h >= kFastH) return PL_OK;
+  if (lines <= 0 || n <= 0) return PL_OK;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  PL_CUDA(cudaStreamIsCapturing(st, &cs));
+  if (cs != cudaStreamCaptureStatusNone)
+    return set_err(PL_ERR_UNSUPPORTED,
+                   "h below the fp32 kernels' bounded range cannot be decided inside a stream "
+                   "capture (set PL_PRECISION_FAST or call outside the capture)");
+  Scratch scratch(st);
+  uint32_t* mm = nullptr;
+  int rc = scratch.alloc(2 * sizeof(uint32_t), &mm);
+  if (rc) return rc;
+  const uint32_t init[2] = {0xFFFFFFFFu, 0u};
+  uint32_t got[2] = {0, 0};
+  PL_CUDA(cudaMemcpyAsync(mm, init, sizeof init, cudaMemcpyHostToDevice, st));
+  const int64_t total = lines * n;
+  const unsigned blocks = (unsigned)std::min<int64_t>((total + 255) / 256, 148 * 8);
+  plgpu::range_kernel<<<blocks, 256, 0, st>>>(src, lines, n, ld, mm);
+  PL_CUDA(cudaMemcpyAsync(got, mm, sizeof got, cudaMemcpyDeviceToHost, st));
+  PL_CUDA(cudaStreamSynchronize(st));
+  if (got[0] > got[1]) return PL_OK;  // no finite sample
+  const double range = (double)plgpu::ordered_value(got[1]) - (double)plgpu::ordered_value(got[0]);
+  *precise = h < kFastH * range / 255.0;
+  return PL_OK;
+}
+
+// fp32 buffers through an fp64 entry point: widen into stream-ordered
+// scratch, `call(src64, dst64, work64)`, narrow.  `work_doubles` = the fp64
+// composite's own workspace.
+template <typename Call>
+int run_precise(const float* src, float* dst, int64_t lines, int32_t n, int64_t ld,
+                size_t work_doubles, cudaStream_t st, Call&& call) {
+  if (lines <= 0) return PL_OK;
+  const int64_t cnt = lines * n;
+  Scratch scratch(st);
+  double* buf = nullptr;
+  int rc = scratch.alloc((2 * (size_t)cnt + work_doubles) * sizeof(double), &buf);
+  if (rc) return rc;
+  const unsigned blocks = (unsigned)std::min<int64_t>((cnt + 255) / 256, 148 * 16);
+  plgpu::widen_kernel<<<blocks, 256, 0, st>>>(src, buf, lines, n, ld);
+  if ((rc = call(buf, buf + cnt, buf + 2 * cnt))) return rc;
+  plgpu::narrow_kernel<<<blocks, 256, 0, st>>>(buf + cnt, dst, lines, n, ld);
+  return check_launch();
+}
+
+// Image composites / passes in double: op 0 RC, 1 CR, 2 S-NLM, 3 row, 4 col.
+int precise_image(int op, const float* src, float* dst, int batch, int rows, int cols,
+                  const pl_params& p, cudaStream_t st) {
+  const size_t img = (size_t)batch * rows * cols;
+  const size_t work = op == 2 ? 2 * img : (op <= 1 ? img : 0);
+  return run_precise(src, dst, (int64_t)batch * rows, cols, cols, work, st,
+                     [&](double* s64, double* d64, double* w64) {
+                       switch (op) {
+                         case 0: return pl_snlm_2d_row_col_f64(s64, d64, w64, batch, rows, cols, p, st);
+                         case 1: return pl_snlm_2d_col_row_f64(s64, d64, w64, batch, rows, cols, p, st);
+                         case 2: return pl_snlm_2d_f64(s64, d64, w64, batch, rows, cols, p, st);
+                         case 3: return pl_nlm_row_pass_f64(s64, d64, batch, rows, cols, p, st);
+                         default: return pl_nlm_col_pass_f64(s64, d64, batch, rows, cols, p, st);
+                       }
+                     });
+}
+
 }  // namespace
 
 namespace {
@@ -490,14 +646,27 @@ extern "C" {
 int pl_abi_version(void) { return PLGPU_ABI_VERSION; }
 
 int pl_debug_set_route(int32_t walker, int32_t lines, int32_t wpc) {
-  if (walker < 0 || walker > 2 || (lines != 0 && lines != 1 && lines != 2) ||
+  if (walker < 0 || walker > 3 || (lines != 0 && lines != 1 && lines != 2) ||
       (wpc != 0 && wpc != 2 && wpc != 8))
-    return set_err(PL_ERR_ARG, "debug route: walker 0..2, lines 0/1/2, wpc 0/2/8");
+    return set_err(PL_ERR_ARG, "debug route: walker 0..3, lines 0/1/2, wpc 0/2/8");
+  g_dbg_fold.store(walker == 3 ? 2 : 0);  // 3: default walkers, 1D lines never folded
+  if (walker == 3) walker = 0;
   g_dbg_walker.store(walker);
   g_dbg_lines.store(lines);
   g_dbg_wpc.store(wpc);
   return PL_OK;
 }
+
+int pl_set_precision_policy(int32_t policy) {
+  if (policy != PL_PRECISION_AUTO && policy != PL_PRECISION_FAST)
+    return set_err(PL_ERR_ARG, "precision policy: PL_PRECISION_AUTO or PL_PRECISION_FAST");
+  g_policy.store(policy);
+  return PL_OK;
+}
+
+int32_t pl_precision_policy(void) { return g_policy.load(); }
+
+double pl_fast_h_threshold(void) { return kFastH; }
 
 const char* pl_last_error(void) { return g_err.c_str(); }
 
@@ -556,6 +725,13 @@ int pl_nlm_lines(const float* src, float* dst, int64_t n_lines, int32_t n, int64
   int rc = validate_params(p, n);
   if (rc) return rc;
   if ((rc = check_ptrs(src, dst))) return rc;
+  bool precise = false;
+  if ((rc = choose_precise(src, n_lines, n, ld, p.h, as_stream(stream), &precise))) return rc;
+  if (precise)
+    return run_precise(src, dst, n_lines, n, ld, 0, as_stream(stream),
+                       [&](double* s64, double* d64, double*) {
+                         return pl_nlm_lines_f64(s64, d64, n_lines, n, n, p, stream);
+                       });
   plgpu::PassDesc g{};
   g.src = src;
   g.dst = dst;
@@ -588,6 +764,10 @@ int pl_nlm_row_pass(const float* src, float* dst, int32_t batch, int32_t rows, i
   if (!rc) rc = validate_params(p, cols);
   if (!rc) rc = check_ptrs(src, dst);
   if (rc) return rc;
+  bool precise = false;
+  if ((rc = choose_precise(src, (int64_t)batch * rows, cols, cols, p.h, as_stream(stream), &precise)))
+    return rc;
+  if (precise) return precise_image(3, src, dst, batch, rows, cols, p, as_stream(stream));
   return run_pass(row_desc(src, dst, batch, rows, cols), p, as_stream(stream));
 }
 
@@ -597,6 +777,10 @@ int pl_nlm_col_pass(const float* src, float* dst, int32_t batch, int32_t rows, i
   if (!rc) rc = validate_params(p, rows);
   if (!rc) rc = check_ptrs(src, dst);
   if (rc) return rc;
+  bool precise = false;
+  if ((rc = choose_precise(src, (int64_t)batch * rows, cols, cols, p.h, as_stream(stream), &precise)))
+    return rc;
+  if (precise) return precise_image(4, src, dst, batch, rows, cols, p, as_stream(stream));
   return run_pass(col_desc(src, dst, batch, rows, cols), p, as_stream(stream));
 }
 
@@ -757,6 +941,10 @@ int pl_snlm_2d_row_col(const float* src, float* dst, float* work, int32_t batch,
   if (!rc) rc = validate_params(p, cols);
   if (!rc) rc = check_ptrs(src, dst);
   if (rc) return rc;
+  bool precise = false;
+  if ((rc = choose_precise(src, (int64_t)batch * rows, cols, cols, p.h, as_stream(stream), &precise)))
+    return rc;
+  if (precise) return precise_image(0, src, dst, batch, rows, cols, p, as_stream(stream));
   Scratch scratch(as_stream(stream));
   if (!work && (rc = scratch.alloc(pl_workspace_bytes(0, batch, rows, cols), &work))) return rc;
   return rc_passes(src, dst, work, batch, rows, cols, p, as_stream(stream));
@@ -782,6 +970,10 @@ int pl_graph_rc_create(const float* src, float* dst, float* work, int32_t batch,
   if (!rc) rc = validate_params(p, cols);
   if (!rc) rc = check_ptrs(src, dst);
   if (rc) return rc;
+  if (g_policy.load(std::memory_order_relaxed) != PL_PRECISION_FAST && p.h < kFastH)
+    return set_err(PL_ERR_UNSUPPORTED,
+                   "graph capture covers the fp32 kernels only: h is below their bounded range "
+                   "(pl_fast_h_threshold); use pl_snlm_2d_row_col or PL_PRECISION_FAST");
   pl_graph* g = new pl_graph();
   auto fail = [&](int code) {
     if (g->exec) cudaGraphExecDestroy(g->exec);
@@ -843,6 +1035,10 @@ int pl_snlm_2d_col_row(const float* src, float* dst, float* work, int32_t batch,
   if (!rc) rc = check_ptrs(src, dst);
   if (rc) return rc;
   cudaStream_t st = as_stream(stream);
+  bool precise = false;
+  if ((rc = choose_precise(src, (int64_t)batch * rows, cols, cols, p.h, as_stream(stream), &precise)))
+    return rc;
+  if (precise) return precise_image(1, src, dst, batch, rows, cols, p, as_stream(stream));
   Scratch scratch(st);
   if (!work && (rc = scratch.alloc(pl_workspace_bytes(1, batch, rows, cols), &work))) return rc;
   if ((rc = run_pass(col_desc(src, work, batch, rows, cols), p, st))) return rc;
@@ -856,6 +1052,10 @@ int pl_snlm_2d(const float* src, float* dst, float* work, int32_t batch, int32_t
   if (!rc) rc = validate_params(p, cols);
   if (!rc) rc = check_ptrs(src, dst);
   if (rc) return rc;
+  bool precise = false;
+  if ((rc = choose_precise(src, (int64_t)batch * rows, cols, cols, p.h, as_stream(stream), &precise)))
+    return rc;
+  if (precise) return precise_image(2, src, dst, batch, rows, cols, p, as_stream(stream));
   Scratch scratch(as_stream(stream));
   if (!work && (rc = scratch.alloc(pl_workspace_bytes(2, batch, rows, cols), &work))) return rc;
   const int64_t cnt = (int64_t)batch * rows * cols;
@@ -863,7 +1063,9 @@ int pl_snlm_2d(const float* src, float* dst, float* work, int32_t batch, int32_t
   float* mid = work + cnt;
   // CR into the workspace, then RC with the average fused into the final
   // column pass's store: dst = (CR + RC) / 2 (average(), nlm.cpp:106-112).
-  if ((rc = pl_snlm_2d_col_row(src, cr_img, mid, batch, rows, cols, p, stream))) return rc;
+  // (the fp32 route is decided: run CR's passes directly, not through its entry point)
+  if ((rc = run_pass(col_desc(src, mid, batch, rows, cols), p, as_stream(stream)))) return rc;
+  if ((rc = run_pass(row_desc(mid, cr_img, batch, rows, cols), p, as_stream(stream)))) return rc;
   return rc_passes(src, dst, mid, batch, rows, cols, p, as_stream(stream), cr_img);
 }
 
@@ -883,6 +1085,18 @@ int pl_snlm_2d_row_col_host(const float* host_src, float* host_dst, int32_t batc
   // first error is returned.
   cudaStream_t st = as_stream(stream);
   const size_t img = (size_t)rows * cols;
+  // precision policy on host data: the range is scanned on the host
+  bool precise = false;
+  if (g_policy.load(std::memory_order_relaxed) != PL_PRECISION_FAST && p.h < kFastH) {
+    float lo = std::numeric_limits<float>::infinity(), hi = -lo;
+    const size_t total = img * batch;
+    for (size_t i = 0; i < total; ++i) {
+      const float v = host_src[i];
+      lo = v < lo ? v : lo;
+      hi = v > hi ? v : hi;
+    }
+    precise = hi >= lo && p.h < kFastH * ((double)hi - (double)lo) / 255.0;
+  }
   const int per = (int)std::max<size_t>(1, std::min<size_t>(batch, (8u << 20) / (img * 4) + 1));
   const int ngroups = (batch + per - 1) / per;
   constexpr int NSLOT = 3;
@@ -921,7 +1135,8 @@ int pl_snlm_2d_row_col_host(const float* host_src, float* host_dst, int32_t batc
                             cudaMemcpyHostToDevice, pipe.s_in));
     PL_CUDA(cudaEventRecord(up[k], pipe.s_in));
     PL_CUDA(cudaStreamWaitEvent(st, up[k], 0));
-    int r = rc_passes(in, out, mid, nb, rows, cols, p, st);
+    int r = precise ? precise_image(0, in, out, nb, rows, cols, p, st)
+                    : rc_passes(in, out, mid, nb, rows, cols, p, st);
     if (r) return r;
     PL_CUDA(cudaEventRecord(done[k], st));
     PL_CUDA(cudaStreamWaitEvent(pipe.s_out, done[k], 0));

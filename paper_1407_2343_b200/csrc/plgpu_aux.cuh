@@ -7,6 +7,8 @@
 //     (nlm.cpp:120-142); also serves radii above the walker's instantiations.
 #pragma once
 
+#include <cstring>
+
 #include <cstdint>
 
 #include "plgpu_walk.cuh"
@@ -233,6 +235,69 @@ __global__ void __launch_bounds__(128) nlm_2d_naive64_kernel(Naive2D64Desc g) {
       vmax = fmax(vmax, v);
     }
   g.dst[w] = fmin(fmax(num / den, vmin), vmax);
+}
+
+
+// ---- precision policy helpers (plgpu.cu: choose_precise / precise_*) --------
+// Order-preserving map float -> uint32 so atomicMin / atomicMax give the
+// range of a buffer (NaNs are skipped).
+__device__ __forceinline__ uint32_t ordered_bits(float f) {
+  const uint32_t u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__host__ __device__ inline float ordered_value(uint32_t o) {
+  const uint32_t u = (o & 0x80000000u) ? (o & 0x7FFFFFFFu) : ~o;
+#ifdef __CUDA_ARCH__
+  return __uint_as_float(u);
+#else
+  float f;
+  memcpy(&f, &u, sizeof f);
+  return f;
+#endif
+}
+
+// Range of `lines` lines of n samples (line l at src + l * ld) into
+// out[0] = ordered min, out[1] = ordered max (preset to ~0u / 0u).
+__global__ void __launch_bounds__(256) range_kernel(const float* __restrict__ src, int64_t lines,
+                                                    int32_t n, int64_t ld, uint32_t* out) {
+  const int64_t total = lines * n;
+  uint32_t lo = 0xFFFFFFFFu, hi = 0u;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float v = ld == n ? src[i] : src[(i / n) * ld + (i % n)];
+    if (v == v) {
+      const uint32_t o = ordered_bits(v);
+      lo = min(lo, o);
+      hi = max(hi, o);
+    }
+  }
+  lo = __reduce_min_sync(0xFFFFFFFFu, lo);
+  hi = __reduce_max_sync(0xFFFFFFFFu, hi);
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(out, lo);
+    atomicMax(out + 1, hi);
+  }
+}
+
+// fp32 lines (stride ld) -> compact fp64 lines (stride n) and back.
+__global__ void __launch_bounds__(256) widen_kernel(const float* __restrict__ src,
+                                                    double* __restrict__ dst, int64_t lines,
+                                                    int32_t n, int64_t ld) {
+  const int64_t total = lines * n;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = (double)(ld == n ? src[i] : src[(i / n) * ld + (i % n)]);
+}
+__global__ void __launch_bounds__(256) narrow_kernel(const double* __restrict__ src,
+                                                     float* __restrict__ dst, int64_t lines,
+                                                     int32_t n, int64_t ld) {
+  const int64_t total = lines * n;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float v = (float)src[i];
+    if (ld == n) dst[i] = v;
+    else dst[(i / n) * ld + (i % n)] = v;
+  }
 }
 
 }  // namespace plgpu

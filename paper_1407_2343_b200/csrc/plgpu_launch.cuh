@@ -35,9 +35,12 @@ constexpr int pass2_lines(int ST) { return ST <= 16 ? 2 : 1; }
 // flush (plgpu_walk3.cuh).
 template <int ST>
 bool launch_pass3(const Pass3Desc& d, int io, cudaStream_t st);
+// Folded 1D pass (plgpu_walk3.cuh, Pass3FoldDesc); lines = lines per lane.
+template <int ST>
+bool launch_pass3_fold(const Pass3FoldDesc& d, int lines, cudaStream_t st);
 constexpr int pass3_k_for(int ST) { return ST == 10 ? 3 : ST == 15 ? 5 : ST == 25 ? 7 : -1; }
 // warps per CTA the configs run with (PLGPU_WPC can override for io 0/1)
-constexpr int pass3_default_wpc(int ST) { return ST >= 15 ? 8 : 2; }
+constexpr int pass3_default_wpc(int ST) { return ST >= 15 ? kLockWpc : 2; }
 
 #ifdef PLGPU_DEFINE_LAUNCHERS
 template <int ST>
@@ -76,10 +79,10 @@ template <int ST, int KT, int L, int IO, int WPC, bool AVG, bool EXP = false>
 void launch3(const Pass3Desc& d, cudaStream_t st) {
   const size_t smem = sizeof(float) * WPC * pass3_smem_floats_per_warp<ST, L, IO>();
   unsigned grid;
-  if constexpr (WPC == 8) {  // 8 line groups of one segment per CTA
+  if constexpr (WPC == kLockWpc) {  // WPC line groups of one segment per CTA
     const int64_t groups = d.b.total_warps / d.b.nseg;
     const int64_t images = groups / d.b.groups_per_img;
-    grid = (unsigned)(images * ((d.b.groups_per_img + 7) / 8) * d.b.nseg);
+    grid = (unsigned)(images * ((d.b.groups_per_img + WPC - 1) / WPC) * d.b.nseg);
   } else {
     grid = (unsigned)((d.b.total_warps + WPC - 1) / WPC);
   }
@@ -105,10 +108,10 @@ bool launch_pass3(const Pass3Desc& d, int io, cudaStream_t st) {
         return;
       }
       if (io == 1) {
-        if (d.wpc == 8) launch3<ST, KT, L, 1, 8, false>(d, st);
+        if (d.wpc == kLockWpc) launch3<ST, KT, L, 1, kLockWpc, false>(d, st);
         else launch3<ST, KT, L, 1, 2, false>(d, st);
       } else if (io == 0 && !d.b.avg) {
-        if (d.wpc == 8) launch3<ST, KT, L, 0, 8, false>(d, st);
+        if (d.wpc == kLockWpc) launch3<ST, KT, L, 0, kLockWpc, false>(d, st);
         else launch3<ST, KT, L, 0, 2, false>(d, st);
       } else if (io == 0) {
         launch3<ST, KT, L, 0, DW, true>(d, st);
@@ -128,8 +131,35 @@ bool launch_pass3(const Pass3Desc& d, int io, cudaStream_t st) {
   }
 }
 
+template <int ST>
+bool launch_pass3_fold(const Pass3FoldDesc& d, int lines, cudaStream_t st) {
+  constexpr int KT = pass3_k_for(ST);
+  if constexpr (KT < 0) {
+    return false;
+  } else {
+    if (d.edge.K != KT || d.edge.S != ST) return false;
+    auto go = [&](auto lines_tag) {
+      constexpr int L = decltype(lines_tag)::value;
+      const size_t smem = sizeof(float) * kWarpsPerCta * pass3_smem_floats_per_warp<ST, L, 1>();
+      const unsigned grid =
+          (unsigned)(d.fold_ctas + (d.edge_warps + kWarpsPerCta - 1) / kWarpsPerCta);
+      auto k = nlm_pass3_fold_kernel<ST, KT, L>;
+      if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      k<<<grid, 32 * kWarpsPerCta, smem, st>>>(d);
+    };
+    if constexpr (ST <= 16) {
+      if (lines == 2) go(std::integral_constant<int, 2>{});
+      else go(std::integral_constant<int, 1>{});
+    } else {
+      go(std::integral_constant<int, 1>{});
+    }
+    return true;
+  }
+}
+
 #define PLGPU_INSTANTIATE(ST)                                              \
   template bool launch_pass3<ST>(const Pass3Desc&, int, cudaStream_t);     \
+  template bool launch_pass3_fold<ST>(const Pass3FoldDesc&, int, cudaStream_t); \
   template void launch_pass<ST>(const PassDesc&, cudaStream_t);            \
   template void launch_pass2<ST>(const Pass2Desc&, bool, cudaStream_t);    \
   template void launch_pass64<ST>(const Pass64Desc&, cudaStream_t);        \

@@ -33,9 +33,21 @@
 #include "plgpu_walk2.cuh"
 
 
+#ifndef PLGPU_PK1
+#define PLGPU_PK1 1  // 1-line kernels: {num, den} packed (FFMA2); 0 = scalar accumulators
+#endif
+
+#ifndef PLGPU_LOCK_WPC
+#define PLGPU_LOCK_WPC 8   // warps per lockstep CTA
+#endif
+#ifndef PLGPU_LOCK_MINB
+#define PLGPU_LOCK_MINB 1  // resident lockstep CTAs per SM the register budget allows
+#endif
+
 namespace plgpu {
 
 constexpr int kNS3 = 4;
+constexpr int kLockWpc = PLGPU_LOCK_WPC;
 
 // Per warp: NS staging chunks + one output chunk, R rows each; rounded up to
 // 16 bytes so every warp's ring (and its 16-byte flush rows) stays aligned.
@@ -260,7 +272,7 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
   // LINES == 1: one line per lane; the numerator/denominator pairs are packed
   // instead, {num, den} += w * {f, 1} being one FFMA2 (w broadcast), and the
   // f ring holds {f, 1} pairs.  Same per-line arithmetic either way.
-  constexpr bool PK = LINES == 1;
+  constexpr bool PK = LINES == 1 && PLGPU_PK1;
   V fr[PK ? 1 : R], an[PK ? 1 : R], ad[PK ? 1 : R];
   V nr[R], orr[R], d[R];
   F2 frp[PK ? R : 1], acc[PK ? R : 1];
@@ -606,15 +618,15 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
 // synchronise once per iteration (named barrier over the active warps).
 template <int ST, int KT, int LINES, int IO, int WPC = kWarpsPerCta, bool AVG = false,
           bool EXP = false>
-__global__ void __launch_bounds__(32 * WPC, 1)
+__global__ void __launch_bounds__(32 * WPC, (WPC == kLockWpc && LINES == 1 && ST <= 16) ? PLGPU_LOCK_MINB : 1)
     nlm_pass3_kernel(const Pass3Desc d) {
   extern __shared__ __align__(16) float smem[];
   const Pass2Desc& g = d.b;
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   float* ring = smem + wib * pass3_smem_floats_per_warp<ST, LINES, IO>();
-  if constexpr (WPC == 8) {
-    const int bpi = (g.groups_per_img + 7) / 8;  // 8-group blocks per image
+  if constexpr (WPC == kLockWpc) {
+    const int bpi = (g.groups_per_img + WPC - 1) / WPC;  // WPC-group blocks per image
     const int64_t blocks_per_seg = (g.total_warps / g.nseg + 0) / g.groups_per_img * bpi;
     const int n_int = pass3_split(ST) ? max(0, d.seg_hi - d.seg_lo + 1) : 0;
     const int64_t int_ctas = (int64_t)n_int * blocks_per_seg;
@@ -635,8 +647,8 @@ __global__ void __launch_bounds__(32 * WPC, 1)
       interior = !pass3_split(ST);
     }
     const int64_t img = blk / bpi;
-    const int gb = (int)(blk % bpi) * 8;
-    const int active = min(8, g.groups_per_img - gb);
+    const int gb = (int)(blk % bpi) * WPC;
+    const int active = min(WPC, g.groups_per_img - gb);
     if (wib >= active) return;
     const int64_t grp = img * g.groups_per_img + gb + wib;
     const int bt = active * 32;
@@ -668,5 +680,48 @@ __global__ void __launch_bounds__(32 * WPC, 1)
     }
   }
 }
+
+// ---- folded 1D pass -----------------------------------------------------------
+// Few, long lines (1D signals: c1 is ONE 65,536-sample line) leave the lane
+// dimension empty when a lane is a line.  Here the lanes of a warp take
+// consecutive SEGMENTS of one real line instead: the interior segments
+// [jlo, jhi] of a line become the "lines" of a virtual image whose line l
+// starts at sample (jlo - 1 + l) * C of the real line (line stride C, length
+// 3C) and whose only processed segment is its second one -- exactly the real
+// segment jlo + l with its pre-walk and halo, all inside the real line, so the
+// walker runs the interior arithmetic unchanged (bitwise the same outputs as
+// one warp per segment).  The segments that touch a line end (mirror, window
+// clipping) run as warps of the same launch on the real lines (`edge`).
+struct Pass3FoldDesc {
+  Pass2Desc fold;     // virtual image per real line (seg_begin = 1, nseg = 1)
+  Pass2Desc edge;     // the real lines; nseg / total_warps count all segments
+  int32_t jlo, jhi;   // folded (interior) segments of every real line
+  int32_t fold_ctas;  // CTAs [0, fold_ctas) run `fold`, the rest `edge`
+  int64_t edge_warps; // real line groups x segments outside [jlo, jhi]
+};
+
+template <int ST, int KT, int LINES>
+__global__ void __launch_bounds__(32 * kWarpsPerCta, 1)
+    nlm_pass3_fold_kernel(const Pass3FoldDesc d) {
+  extern __shared__ __align__(16) float smem[];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  float* ring = smem + wib * pass3_smem_floats_per_warp<ST, LINES, 1>();
+  constexpr int MI = pass3_split(ST) ? 1 : 0;  // interior-only body for large S
+  constexpr int ME = pass3_split(ST) ? 2 : 0;
+  if ((int)blockIdx.x < d.fold_ctas) {
+    const int64_t wid = (int64_t)blockIdx.x * kWarpsPerCta + wib;
+    if (wid >= d.fold.total_warps) return;
+    walk3<ST, KT, LINES, 1, MI>(d.fold, ring, lane, wid, d.fold.seg_begin);
+  } else {
+    const int64_t e = ((int64_t)blockIdx.x - d.fold_ctas) * kWarpsPerCta + wib;
+    if (e >= d.edge_warps) return;
+    const int n_edge = d.edge.nseg - (d.jhi - d.jlo + 1);
+    int sidx = (int)(e % n_edge);
+    if (sidx >= d.jlo) sidx += d.jhi - d.jlo + 1;
+    walk3<ST, KT, LINES, 1, ME>(d.edge, ring, lane, e / n_edge, d.edge.seg_begin + sidx);
+  }
+}
+
 
 }  // namespace plgpu

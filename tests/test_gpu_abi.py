@@ -227,3 +227,50 @@ def test_bench_multi_rank_logic_gloo(tmp_path):
     assert forms["slab"]["bitwise_equal_single_gpu_rc"] is True
     assert forms["halo"]["bitwise_equal_single_gpu_rc"] is True
     assert "unavailable" in forms["fused"]
+
+
+@pytest.mark.parametrize("lines,n,S,K", [
+    (1, 65536, 10, 3),   # config c1's shape
+    (3, 40000, 15, 5),
+    (2, 70001, 25, 7),   # interior-only / edge-only bodies (S > 16)
+    (1, 5000, 10, 3),    # ~480-sample segments: 8 folded + 3 edge segments
+    (5, 9000, 15, 5),
+    (31, 33000, 10, 3),  # just under one lane per line
+])
+def test_folded_1d_lines_bitwise(lines, n, S, K):
+    """Few long lines (1D signals) run the hot kernel with the interior
+    SEGMENTS of a line folded onto the lanes (route "hot-fold<...>",
+    plgpu_walk3.cuh Pass3FoldDesc).  Same per-segment arithmetic: bitwise equal
+    to the unfolded routes (walker 3 = folding off: one warp per segment from 16
+    lines, the portable walker below) and to the portable walker,
+    and within T2 of the oracle (nlm_1d_patchlift, nlm.cpp:144-166)."""
+    from oracle import Oracle
+    rng = np.random.default_rng(lines * 1000 + S)
+    x = rng.uniform(0, 255, (lines, n)).astype(np.float32)
+    p = (S, K, 60.0)
+    xd = dev(x)
+    y = host(pl.nlm_1d_patchlift(xd, p))
+    assert pl.last_route().startswith(f"hot-fold<S={S},K={K},"), pl.last_route()
+    with pl.debug_route(3):
+        y_unfolded = host(pl.nlm_1d_patchlift(xd, p))  # hot kernel from 16 lines, else portable
+        assert pl.last_route().startswith("hot<" if lines >= 16 else "portable<"), pl.last_route()
+    with pl.debug_route(1):
+        y_portable = host(pl.nlm_1d_patchlift(xd, p))
+    assert np.array_equal(y, y_unfolded)
+    assert np.array_equal(y, y_portable)
+    want = Oracle.get().nlm_1d(x[lines - 1].astype(np.float64), S, K, 60.0)
+    assert np.abs(y[lines - 1].astype(np.float64) - want).max() <= 1e-3
+
+
+def test_folded_image_rows_with_few_rows():
+    """A row pass over images of a few very long rows folds too (each row is
+    its own virtual image); many rows do not."""
+    rng = np.random.default_rng(77)
+    x = rng.uniform(0, 255, (2, 6, 36000)).astype(np.float32)
+    p = (10, 3, 70.0)
+    y = host(pl.nlm_row_pass(dev(x), p))
+    assert pl.last_route().startswith("hot-fold<"), pl.last_route()
+    with pl.debug_route(3):
+        assert np.array_equal(y, host(pl.nlm_row_pass(dev(x), p)))
+    pl.nlm_row_pass(dev(rng.uniform(0, 255, (1, 64, 4000)).astype(np.float32)), p)
+    assert pl.last_route().startswith("hot<"), pl.last_route()

@@ -166,28 +166,103 @@ def test_images_vs_oracle(orc):
                 assert np.abs(got - want).max() <= T2, (r, c, S, K, op)
 
 
-def test_small_h_conditioning(orc):
-    """Small h on 8-bit data.  The fp32 moving sums carry an absolute rounding
-    error ~ ulp(max d') that grows like 1/h^2 (d' = d log2(e) / h^2 reaches
-    thousands for dissimilar patches), and a two-pass composite also
-    amplifies the first pass's output rounding by the second pass's
-    condition number (~ 2 |df| |f - out| / h^2).  Single passes are held to
-    T2 (25/h)^2, composites to T2 (32/h)^2 below those h; both are T2 for the
-    configs (h >= 74.8).  Measured worst over ~25,000 random cases
-    (tools/fuzz_parity.py): 0.84 and 0.65 of these bounds."""
+def test_small_h_strict_t2_default_policy(orc):
+    """Small h on 8-bit data, default precision policy (PL_PRECISION_AUTO):
+    every reference-API filter holds the strict T2 = 1e-3 against the oracle
+    at any h.  Below pl_fast_h_threshold() (40 per 255 of data range) the
+    library measures the input's range and runs the call in double on the
+    device (route "f64<...>"); the host-buffer pipeline follows the same rule."""
     rng = np.random.default_rng(41)
+    assert pl.fast_h_threshold() == 40.0
     for t in range(12):
         r, c = int(rng.integers(20, 200)), int(rng.integers(20, 200))
         S, K = int(rng.integers(2, 26)), int(rng.integers(0, 3))
-        h = float(rng.uniform(5.0, 25.0))
+        h = float(rng.uniform(5.0, 39.0))
         img = rng.uniform(0, 255, (r, c)).astype(np.float32)
         x = dev(img)
         for op, fn in (("row", pl.nlm_row_pass), ("col", pl.nlm_col_pass),
-                       ("rc", pl.snlm_2d_row_col), ("cr", pl.snlm_2d_col_row)):
+                       ("rc", pl.snlm_2d_row_col), ("cr", pl.snlm_2d_col_row),
+                       ("snlm", pl.snlm_2d)):
             want = orc.filter(op, img.astype(np.float64), S, K, h, threads=4)
             err = np.abs(host(fn(x, (S, K, h))).astype(np.float64) - want).max()
-            tol = T2 * max(1.0, ((25.0 if op in ("row", "col") else 32.0) / h) ** 2)
-            assert err <= tol, (op, r, c, S, K, h, err)
+            assert pl.last_route().startswith("f64"), (op, pl.last_route())
+            assert err <= T2, (op, r, c, S, K, h, err)
+        if t < 4:
+            want = orc.filter("rc", img.astype(np.float64), S, K, h, threads=4)
+            got = pl.snlm_2d_row_col_host(img[None], (S, K, h))
+            assert np.abs(np.asarray(got)[0].astype(np.float64) - want).max() <= T2, (r, c, S, K, h)
+    # 1D lines through the same policy; with a line stride ld > n via the C ABI
+    n, S, K, h = 700, 10, 3, 9.0
+    sig = rng.uniform(0, 255, (5, n)).astype(np.float32)
+    got = host(pl.nlm_1d_patchlift(dev(sig), (S, K, h)))
+    assert pl.last_route().startswith("f64")
+    padded = np.full((5, n + 3), 1e9, np.float32)  # the padding must not widen the measured range
+    padded[:, :n] = sig
+    xp = dev(padded)
+    yp = torch.full_like(xp, -7.0)
+    pl._check(pl.lib().pl_nlm_lines(xp.data_ptr(), yp.data_ptr(), 5, n, n + 3,
+                                    pl._params((S, K, h)), pl._stream(xp)))
+    yp = host(yp)
+    assert np.all(yp[:, n:] == -7.0)
+    for l in range(5):
+        want = orc.nlm_1d(sig[l].astype(np.float64), S, K, h)
+        assert np.abs(got[l].astype(np.float64) - want).max() <= T2
+        assert np.array_equal(yp[l, :n], got[l])
+
+
+def test_precision_policy_routes(orc):
+    """The policy is scale-aware and never touches the configs' settings:
+    h >= 40 goes straight to the fp32 kernels (no range measurement), a small
+    h on small-range data stays on them (h / range decides), PL_PRECISION_FAST
+    pins them, and a CUDA graph (fp32 only) refuses an h it cannot bound."""
+    rng = np.random.default_rng(43)
+    img = rng.uniform(0, 255, (96, 130)).astype(np.float32)
+    x = dev(img)
+    pl.snlm_2d_row_col(x, (10, 3, 74.8))
+    assert not pl.last_route().startswith("f64"), pl.last_route()
+    pl.snlm_2d_row_col(x, (10, 3, 12.0))
+    assert pl.last_route().startswith("f64"), pl.last_route()
+    # the same image on a [0, 1] scale with h scaled alike is the same problem:
+    # unit-range data with h = 0.3 (= 76.5 per 255) is a fast-route call
+    unit = (img / 255.0).astype(np.float32)
+    got = host(pl.snlm_2d_row_col(dev(unit), (10, 3, 0.3)))
+    assert not pl.last_route().startswith("f64"), pl.last_route()
+    want = orc.filter("rc", unit.astype(np.float64), 10, 3, 0.3, threads=4)
+    assert np.abs(got.astype(np.float64) - want).max() <= T2 / 255.0
+    with pl.precision_policy("fast"):
+        fast = host(pl.snlm_2d_row_col(x, (10, 3, 12.0)))
+        assert not pl.last_route().startswith("f64"), pl.last_route()
+        g = pl.RCGraph(x, (10, 3, 12.0))  # allowed when pinned fast
+        del g
+    with pytest.raises(RuntimeError, match="graph capture covers the fp32 kernels only"):
+        pl.RCGraph(x, (10, 3, 12.0))
+    # fp32 characterisation (what the policy protects from): the fast route's
+    # error at small h stays within T2 (25/h)^2 single pass / (32/h)^2 composite
+    want = orc.filter("rc", img.astype(np.float64), 10, 3, 12.0, threads=4)
+    assert np.abs(fast.astype(np.float64) - want).max() <= T2 * (32.0 / 12.0) ** 2
+
+
+def test_small_h_fast_policy_bounds(orc):
+    """PL_PRECISION_FAST at small h (the fp32 kernels' own behaviour).  The fp32
+    moving sums carry an absolute rounding error ~ ulp(max d') that grows like
+    1/h^2, and a two-pass composite amplifies the first pass's output rounding
+    by the second pass's condition number (~ 2 |df| |f - out| / h^2): single
+    passes stay within T2 (25/h)^2, composites within T2 (32/h)^2 (worst over
+    ~25,000 random cases, tools/fuzz_parity.py: 0.84 and 0.65 of these)."""
+    rng = np.random.default_rng(41)
+    with pl.precision_policy("fast"):
+        for t in range(12):
+            r, c = int(rng.integers(20, 200)), int(rng.integers(20, 200))
+            S, K = int(rng.integers(2, 26)), int(rng.integers(0, 3))
+            h = float(rng.uniform(5.0, 25.0))
+            img = rng.uniform(0, 255, (r, c)).astype(np.float32)
+            x = dev(img)
+            for op, fn in (("row", pl.nlm_row_pass), ("col", pl.nlm_col_pass),
+                           ("rc", pl.snlm_2d_row_col), ("cr", pl.snlm_2d_col_row)):
+                want = orc.filter(op, img.astype(np.float64), S, K, h, threads=4)
+                err = np.abs(host(fn(x, (S, K, h))).astype(np.float64) - want).max()
+                tol = T2 * max(1.0, ((25.0 if op in ("row", "col") else 32.0) / h) ** 2)
+                assert err <= tol, (op, r, c, S, K, h, err)
 
 
 def test_golden_images_t2(golden):
