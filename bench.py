@@ -393,7 +393,7 @@ def torch_cat(parts):
     return torch.cat(parts, 0)
 
 
-def timed_graph(D, first_pass, second_pass, steps, warmup):
+def timed_graph(D, first_pass, second_pass, steps, warmup, has_second=True):
     """Launch-bound configs (c1: one ~10 us kernel per step; c2: two): the K
     timed steps are captured into ONE CUDA graph and replayed with a single
     launch, so the events bracket device time and not the Python/ctypes launch
@@ -424,12 +424,13 @@ def timed_graph(D, first_pass, second_pass, steps, warmup):
         return a.elapsed_time(b) / steps
 
     eager = timed(D, first_pass, second_pass, steps, warmup, clocks=False)
-    g_all, g_row, g_col = capture([first_pass, second_pass]), capture([first_pass]), capture([second_pass])
+    g_all, g_row = capture([first_pass, second_pass]), capture([first_pass])
+    g_col = capture([second_pass]) if has_second else None
     sampler = ClockSampler(D.dev.index)
     sampler.__enter__()
     try:
         ms_step = D.max(replay_ms(g_all))
-        row_ms, col_ms = replay_ms(g_row), replay_ms(g_col)
+        row_ms, col_ms = replay_ms(g_row), (replay_ms(g_col) if g_col else 0.0)
         if len(sampler.lines) < 3:
             time.sleep(0.35)
     finally:
@@ -805,7 +806,8 @@ def run_ours(args):
             lo, hi = shard(n_items, world, rank)
         run = BatchRun(D, pl, args.config, lo, hi, params)
         if args.config in ("c1", "c2") and world == 1 and not args.no_graph:
-            t = timed_graph(D, run.first_pass, run.second_pass, args.steps, args.warmup)
+            t = timed_graph(D, run.first_pass, run.second_pass, args.steps, args.warmup,
+                            has_second=not run.signal)
         else:
             t = timed(D, run.first_pass, run.second_pass, args.steps, args.warmup)
         px_total = c["n"] if run.signal else n_items * c["rows"] * c["cols"]

@@ -238,6 +238,7 @@ int try_pass2(const plgpu::PassDesc& g, cudaStream_t st) {
   d.K = g.K;
   d.coef = g.coef;
   d.scale = g.scale;
+  d.inv_scale = g.inv_scale;
   d.nx = g.nx;
   for (int x = 0; x < 2; ++x) {
     d.xdst[x] = g.xdst[x];
@@ -394,6 +395,7 @@ int run_pass(plgpu::PassDesc g, const pl_params& p, cudaStream_t st) {
   g.coef = weight_coef(p.h);
   // debug distance export: the recurrence on raw samples (exact on integers)
   g.scale = g.dexp ? 1.0f : static_cast<float>(std::sqrt(1.4426950408889634) / p.h);
+  g.inv_scale = static_cast<float>(1.0 / static_cast<double>(g.scale));  // acc_prescaled unscale
   g.seg_len = segment_length(g.n, g.S);
   if (g.nseg <= 0) {  // whole lines (windowed passes preset seg_begin / nseg)
     g.seg_begin = 0;

@@ -60,7 +60,8 @@ struct PassDesc {
   int32_t seg_len;  // C
   int32_t nseg;     // segments processed (ceil(n / C) unless windowed)
   int32_t seg_begin;  // index of the first processed segment (windowed passes)
-  float scale;        // sqrt(log2 e) / h: distance-side sample prescale
+  float scale;        // s = sqrt(log2 e) / h: sample prescale
+  float inv_scale;    // 1 / s (double division, rounded once): acc_prescaled output unscale
   const float* avg;   // optional, dst layout: store (avg + out) / 2 (snlm_2d's average)
   int32_t S;        // effective search radius, <= template S, <= n-1
   int32_t K;        // patch radius
@@ -99,6 +100,21 @@ __device__ __forceinline__ float div_fix(float num, float den) {
   float r;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(den));
   return num * r;
+}
+
+// Accumulation form (shared rule of all walkers, a function of the template
+// radius ST alone, like the clamp range below).  For ST <= 10 the filters
+// accumulate PRESCALED samples: num = sum of w x' with x' = s f, the values the
+// distance rings already hold, so the 2-line hot kernel keeps no separate f
+// ring (22 registers and one LDS.64 per step less: c4 +1.5 %); den = sum of w
+// as before and the output is num * (rcp(den) * (1 / s)).  Larger radii (the
+// 1-line packed kernels, where the extra multiplies cost c3 2.3 %) accumulate
+// the raw samples: num * rcp(den).
+__host__ __device__ constexpr bool acc_prescaled(int ST) { return ST <= 10; }
+__device__ __forceinline__ float div_unscale(float num, float den, float inv_s) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(den));
+  return __fmul_rn(num, __fmul_rn(r, inv_s));
 }
 
 // Three-input min / max (FMNMX3).  The clamp range of every walker is built
@@ -147,6 +163,7 @@ __device__ __forceinline__ void walk_segment(const PassDesc& g, const float* __r
                                              int64_t ps, float* __restrict__ dst, int64_t dps,
                                              int s0, int s1, float* x0 = nullptr, float* x1 = nullptr) {
   constexpr int R = ST + 1;
+  constexpr bool AP = acc_prescaled(ST);
   const int n = g.n;
   const int S = EDGE ? g.S : ST;
   const int K = g.K;
@@ -173,9 +190,10 @@ __device__ __forceinline__ void walk_segment(const PassDesc& g, const float* __r
 
 #pragma unroll
   for (int q = 0; q < R; ++q) {
-    fr[q] = ld(i0 + q);
-    lo = fminf(lo, fr[q]);
-    hi = fmaxf(hi, fr[q]);
+    const float f0 = ld(i0 + q);
+    lo = fminf(lo, f0);
+    hi = fmaxf(hi, f0);
+    fr[q] = AP ? __fmul_rn(f0, sc) : f0;
     nr[q] = lds(i0 + K + q);
     orr[q] = lds(i0 - 1 - K + q);
     an[q] = fr[q];  // the centre sample (w = 1) starts each pixel's sums
@@ -237,7 +255,8 @@ __device__ __forceinline__ void walk_segment(const PassDesc& g, const float* __r
         ad[rk] += w;
       }
       if (i >= s0) {
-        const float v = epi(g.avg, g.dst, op, fminf(fmaxf(div_fix(num, den), lo), hi));
+        const float q = AP ? div_unscale(num, den, g.inv_scale) : div_fix(num, den);
+        const float v = epi(g.avg, g.dst, op, fminf(fmaxf(q, lo), hi));
         *op = v;
         if (x0) x0[(int64_t)i * dps] = v;  // fan-out (unblocked layout only)
         if (x1) x1[(int64_t)i * dps] = v;
@@ -247,7 +266,8 @@ __device__ __forceinline__ void walk_segment(const PassDesc& g, const float* __r
           orem = blk;
         }
       }
-      an[r] = tf;  // pixel i + R enters slot r: centre term first
+      const float tfs = AP ? __fmul_rn(tf, sc) : tf;
+      an[r] = tfs;  // pixel i + R enters slot r: centre term first
       ad[r] = 1.f;
       if (!pairs) {
         lo = fminf(lo, tf);
@@ -261,7 +281,7 @@ __device__ __forceinline__ void walk_segment(const PassDesc& g, const float* __r
       } else {
         xprev = tx;
       }
-      fr[r] = tf;
+      fr[r] = tfs;
       nr[r] = tn;
       orr[r] = to;
     }

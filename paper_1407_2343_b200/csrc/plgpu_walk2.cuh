@@ -69,6 +69,14 @@ struct VecOps<1> {
   static __device__ __forceinline__ float lo(V a) { return a; }
   static __device__ __forceinline__ float hi(V a) { return a; }
   static __device__ __forceinline__ V div(V n, V d) { return div_fix(n, d); }
+  static __device__ __forceinline__ V div_unscale(V n, V d, float inv_s) {
+    return plgpu::div_unscale(n, d, inv_s);
+  }
+  static __device__ __forceinline__ V rcp(V a) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(a));
+    return r;
+  }
   static __device__ __forceinline__ V lds(const float* p) { return *p; }
 };
 
@@ -150,6 +158,11 @@ struct VecOps<2> {
     const V r = rcp(d);
     return mul(n, r);
   }
+  // num * (rcp(den) * (1/s)): plgpu_walk.cuh div_unscale per half
+  static __device__ __forceinline__ V div_unscale(V n, V d, float inv_s) {
+    return mul(n, mul(rcp(d), splat(inv_s)));
+  }
+
   static __device__ __forceinline__ V lds(const float* p) {
     V o;
     o.r = *reinterpret_cast<const unsigned long long*>(p);
@@ -186,7 +199,8 @@ struct Pass2Desc {
   int32_t groups_per_img;
   int32_t n, seg_len, nseg, S, K;
   int32_t seg_begin;  // first processed segment (windowed passes; nseg counts from it)
-  float scale;        // sqrt(log2 e) / h: distance-side sample prescale
+  float scale;        // s = sqrt(log2 e) / h: sample prescale
+  float inv_scale;    // 1 / s: output unscale where acc_prescaled(ST) (plgpu_walk.cuh)
   const float* avg;   // optional, dst layout (column passes): store (avg + out) / 2
   int32_t vec16;  // column pass: 16-byte copies legal (aligned, full line groups)
   int64_t total_warps;
@@ -296,6 +310,7 @@ __device__ __forceinline__ void walk2(const Pass2Desc& g, float* ring, const int
 
   // Sample rings fr/nr/orr[(s+q) mod R] = samples at u = s+1+K+q, s+1+2K+q,
   // s+q; the distance-side rings nr/orr hold prescaled samples (plgpu_walk.cuh).
+  constexpr bool AP = acc_prescaled(ST);
   V fr[R], nr[R], orr[R];
   V an[R], ad[R], d[R];
   const V zero = Ops::splat(0.f);
@@ -316,7 +331,7 @@ __device__ __forceinline__ void walk2(const Pass2Desc& g, float* ring, const int
   V xprev = zero;
 #pragma unroll
   for (int q = 0; q < R; ++q) {
-    fr[q] = ld(q + 1 + K);
+    fr[q] = AP ? lds(q + 1 + K) : ld(q + 1 + K);  // accumulation side (plgpu_walk.cuh rule)
     nr[q] = lds(q + 1 + 2 * K);
     orr[q] = lds(q);
     d[q] = zero;
@@ -324,7 +339,7 @@ __device__ __forceinline__ void walk2(const Pass2Desc& g, float* ring, const int
   const V one = Ops::splat(1.f);
 #pragma unroll
   for (int q = 0; q < R; ++q) {
-    track(fr[q]);
+    track(ld(q + 1 + K));
     an[q] = fr[q];  // the centre sample (w = 1) starts each pixel's sums
     ad[q] = one;
   }
@@ -402,7 +417,7 @@ __device__ __forceinline__ void walk2(const Pass2Desc& g, float* ring, const int
       }
       const int o = i - s0;
       if (o >= 0) {
-        const V qv = Ops::div(num, den);
+        const V qv = AP ? Ops::div_unscale(num, den, g.inv_scale) : Ops::div(num, den);
         const float o0 = fminf(fmaxf(Ops::lo(qv), lo0), hi0);
         float o1 = o0;
         if constexpr (LINES == 2) o1 = fminf(fmaxf(Ops::hi(qv), lo1), hi1);
@@ -432,13 +447,14 @@ __device__ __forceinline__ void walk2(const Pass2Desc& g, float* ring, const int
           op += g.dst_pos_stride;
         }
       }
-      an[ra] = tf;  // pixel i + R enters slot ra: centre term first
+      const V tfs = AP ? Ops::scale(tf, g.scale) : tf;
+      an[ra] = tfs;  // pixel i + R enters slot ra: centre term first
       ad[ra] = one;
       if (!pairs) track(tf);
       else if (ra & 1) track2(xprev, tx);
       else if (ra == R - 1) track(tx);
       else xprev = tx;
-      fr[ra] = tf;
+      fr[ra] = tfs;
       nr[ra] = tn;
       orr[ra] = to;
       issue_piece((s >> 4) + 2, s & 15);

@@ -37,6 +37,9 @@
 #define PLGPU_PK1 1  // 1-line kernels: {num, den} packed (FFMA2); 0 = scalar accumulators
 #endif
 
+#ifndef PLGPU_PK_REFILL_RING
+#define PLGPU_PK_REFILL_RING 1  // packed 1-line form: refill {x', s} from the nr ring (else LDS + scale)
+#endif
 #ifndef PLGPU_LOCK_WPC
 #define PLGPU_LOCK_WPC 8   // warps per lockstep CTA
 #endif
@@ -273,7 +276,13 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
   // instead, {num, den} += w * {f, 1} being one FFMA2 (w broadcast), and the
   // f ring holds {f, 1} pairs.  Same per-line arithmetic either way.
   constexpr bool PK = LINES == 1 && PLGPU_PK1;
-  V fr[PK ? 1 : R], an[PK ? 1 : R], ad[PK ? 1 : R];
+  // Accumulation form (plgpu_walk.cuh acc_prescaled, a function of ST): for
+  // ST <= 10 the sums take the prescaled samples x' -- the sample at position
+  // i + k is already in the distance rings, so the 2-line kernel keeps no
+  // separate f ring (22 registers and one LDS.64 per step less, c4 +1.5 %) and
+  // the packed 1-line form keeps {x', 1} pairs; larger radii keep the raw f.
+  constexpr bool AP = acc_prescaled(ST);
+  V fr[(PK || AP) ? 1 : R], an[PK ? 1 : R], ad[PK ? 1 : R];
   V nr[R], orr[R], d[R];
   F2 frp[PK ? R : 1], acc[PK ? R : 1];
   const V zero = Ops::splat(0.f);
@@ -302,12 +311,14 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
     orr[q] = sc(ld_init(q));
     d[q] = zero;
     const V f = ld_init(q + 1 + KT);
+    V fa = f;  // accumulation-side sample
+    if constexpr (AP) fa = sc(f);
     if constexpr (PK) {  // the centre sample (w = 1) starts each pixel's sums
-      frp[q] = f2_make(Ops::lo(f), 1.f);
+      frp[q] = f2_make(Ops::lo(fa), 1.f);
       acc[q] = frp[q];
     } else {
-      fr[q] = f;
-      an[q] = f;
+      if constexpr (!AP) fr[q] = fa;
+      an[q] = fa;
       ad[q] = Ops::splat(1.f);
     }
     track(f);
@@ -405,14 +416,21 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
           }
           float qn, qd;
           f2_split(nd, qn, qd);
-          qv = div_fix(qn, qd);
+          qv = AP ? div_unscale(qn, qd, g.inv_scale) : div_fix(qn, qd);
         } else {
-          const V fi = fr[r];
+          // accumulation-side sample at position i + k: the prescaled one sits
+          // in the distance rings (AP), else the f ring
+          auto fsc = [&](int k) -> V {
+            if constexpr (AP) return k >= KT ? nr[(r + k - KT) % R] : orr[(r + k + KT + 1) % R];
+            else return fr[AP ? 0 : (r + k) % R];
+          };
+          const V fi = fsc(0);
           V num = an[r];  // centre + j-side contributions so far
           V den = ad[r];
 #pragma unroll
           for (int k = 1; k <= ST; ++k) {
             const int rk = (r + k) % R;
+            const V fk = fsc(k);
             const V dn = Ops::sub(an_, nr[rk]);
             V dk = Ops::fma(dn, dn, d[k]);
             const V dq = Ops::sub(ao, orr[rk]);
@@ -421,17 +439,17 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
             dexport(i, k, MASK ? kmax : min(S, n - 1 - i), dk);
             V w = Ops::ex2n(dk);
             if constexpr (MASK) w = Ops::zero_if(k > kmax, w);
-            num = Ops::fma(w, fr[rk], num);
+            num = Ops::fma(w, fk, num);
             den = Ops::add(w, den);
             if (k == ST) {  // first contribution to the slot recycled at step r-1,
-              an[rk] = Ops::fma(w, fi, fr[rk]);  // onto its centre term: the portable
-              ad[rk] = Ops::add(w, one);         // walker's fma(w, fi, f) and 1 + w
+              an[rk] = Ops::fma(w, fi, fk);  // onto its centre term: the portable
+              ad[rk] = Ops::add(w, one);     // walker's fma(w, f_i, f) and 1 + w
             } else {
               an[rk] = Ops::fma(w, fi, an[rk]);
               ad[rk] = Ops::add(w, ad[rk]);
             }
           }
-          qv = Ops::div(num, den);
+          qv = AP ? Ops::div_unscale(num, den, g.inv_scale) : Ops::div(num, den);
         }
         const float o0 = fminf(fmaxf(Ops::lo(qv), lo0), hi0);
         float o1 = o0;
@@ -443,14 +461,24 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
           if constexpr (LINES == 2) *reinterpret_cast<float2*>(sl) = make_float2(o0, o1);
           else *sl = o0;
         }
-        // refill slot r in place: first read at step r+1's last offset
-        const V fnew = at(r, 2 + KT + ST);
-        if constexpr (!PAIR) track(fnew);
-        // {f, 1}: keeping the 1.0 half in place measured c3 +1.4 %, c5 -22 % (register
-        // allocation at 255 registers), so only for S <= 16
-        if constexpr (PK && ST <= 16) frp[r] = f2_set_lo(frp[r], Ops::lo(fnew));
-        else if constexpr (PK) frp[r] = f2_make(Ops::lo(fnew), 1.f);
-        else fr[r] = fnew;
+        // refill slot r in place (position i + ST + 1): first read at step r+1's last offset
+        if constexpr (AP) {
+          if constexpr (!PAIR) track(at(r, 2 + KT + ST));
+          if constexpr (PK) {  // x' at position i + ST + 1: in the nr ring for K >= 1
+            float fs1;
+            if constexpr (KT >= 1 && PLGPU_PK_REFILL_RING) fs1 = Ops::lo(nr[(r + ST + 1 - KT) % R]);
+            else fs1 = Ops::lo(sc(at(r, 2 + KT + ST)));
+            frp[r] = f2_set_lo(frp[r], fs1);
+          }
+        } else {
+          const V fnew = at(r, 2 + KT + ST);
+          if constexpr (!PAIR) track(fnew);
+          // {f, 1}: keeping the 1.0 half in place measured c3 +1.4 %, c5 -22 % (register
+          // allocation at 255 registers), so only for S <= 16
+          if constexpr (PK && ST <= 16) frp[r] = f2_set_lo(frp[r], Ops::lo(fnew));
+          else if constexpr (PK) frp[r] = f2_make(Ops::lo(fnew), 1.f);
+          else fr[r] = fnew;
+        }
         // The leaving-term partner entering now (coordinate s+1+ST) entered
         // the nr ring 2K+1 steps ago and is still there when 2K < S: it is
         // copied from the nr ring (2-line

@@ -776,7 +776,7 @@ def test_f64_route_matches_reference_library(ref):
 
 def test_small_h_f64_route_strict(ref):
     """Small h (5..25 on 8-bit data), where the fp32 running sums lose
-    accuracy (test_small_h_conditioning): the fp64 route holds the reference
+    accuracy (test_small_h_fast_policy_bounds): the fp64 route holds the reference
     to 1e-9 -- far inside T2 -- for single passes and composites alike."""
     rng = np.random.default_rng(55)
     for t in range(8):
