@@ -156,6 +156,18 @@ Staging& staging() {
   return s;
 }
 
+// Device results are checked for finiteness while they are copied out (in
+// parallel, run_device / run_device64); when that scan passed, wrapping them
+// into an Image2D skips the single-threaded scan of the public constructor
+// (core_types.cpp:20-47).  A non-finite result still goes through it and
+// raises the reference's ValidationError.
+thread_local bool t_trusted_values = false;
+thread_local bool t_last_result_finite = false;  // set by run_device / run_device64
+struct TrustedValues {
+  explicit TrustedValues(bool finite) { t_trusted_values = finite; }
+  ~TrustedValues() { t_trusted_values = false; }
+};
+
 // double -> fp32 into pinned memory, H2D, `launch(src, dst, stream)`, D2H,
 // fp32 -> double.  Outputs are convex combinations of the inputs
 // (acceptance_main.cpp:255-283): rounding an extreme input to fp32 can move
@@ -189,12 +201,17 @@ std::vector<double> run_device(const std::vector<double>& in, int threads, Launc
   check(pl_copy_to_host_async(h, dst, n * sizeof(float), s));
   check(pl_stream_synchronize(s));
   std::vector<double> out(n);
+  std::atomic<bool> finite{true};
   parallel_chunks(n, threads, [&](std::size_t a, std::size_t b, unsigned) {
+    bool ok = true;
     for (std::size_t i = a; i < b; ++i) {
       const double v = static_cast<double>(h[i]);
+      ok &= std::isfinite(v);
       out[i] = v < lo ? lo : (v > hi ? hi : v);
     }
+    if (!ok) finite.store(false, std::memory_order_relaxed);
   });
+  t_last_result_finite = finite.load();
   return out;
 }
 
@@ -219,9 +236,17 @@ std::vector<double> run_device64(const std::vector<double>& in, int threads, std
   check(pl_copy_to_host_async(h, dst, bytes, s));
   check(pl_stream_synchronize(s));
   std::vector<double> out(n);
+  std::atomic<bool> finite{true};
   parallel_chunks(n, threads, [&](std::size_t a, std::size_t b, unsigned) {
-    std::memcpy(out.data() + a, h + a, (b - a) * sizeof(double));
+    bool ok = true;
+    for (std::size_t i = a; i < b; ++i) {
+      const double v = h[i];
+      ok &= std::isfinite(v);
+      out[i] = v;
+    }
+    if (!ok) finite.store(false, std::memory_order_relaxed);
   });
+  t_last_result_finite = finite.load();
   return out;
 }
 
@@ -231,6 +256,7 @@ bool fp64() { return g_precision.load(std::memory_order_relaxed) == static_cast<
 pl_params to_pl(const NlmParams& p) { return pl_params{p.search_radius, p.patch_radius, p.h}; }
 
 void require_finite(const std::vector<double>& values, const char* what) {
+  if (t_trusted_values) return;
   for (double v : values)
     if (!std::isfinite(v)) throw ValidationError(std::string(what) + " contains a non-finite value");
 }
@@ -265,6 +291,7 @@ Image2D run_image(const Image2D& img, const NlmParams& p, Op op, int threads) {
           }
           return static_cast<int>(PL_ERR_ARG);
         });
+    const TrustedValues trusted(t_last_result_finite);
     return Image2D(R, C, std::move(out));
   }
   std::vector<double> out = run_device(img.data, threads, [&](float* src, float* dst, void* s) {
@@ -278,6 +305,7 @@ Image2D run_image(const Image2D& img, const NlmParams& p, Op op, int threads) {
     }
     return static_cast<int>(PL_ERR_ARG);
   });
+  const TrustedValues trusted(t_last_result_finite);
   return Image2D(R, C, std::move(out));
 }
 
