@@ -209,8 +209,13 @@ int pl_snlm_2d(const float* src, float* dst, float* work, int32_t batch, int32_t
                int32_t cols, pl_params p, void* stream);
 
 /* End-to-end form of pl_snlm_2d_row_col over HOST buffers (pinned or
- * pageable): the H2D copy, both passes and the D2H copy run on `stream`,
- * chunked by image so copies overlap compute.  Blocks until done. */
+ * pageable): H2D copies, both passes and D2H copies are pipelined on `stream`
+ * and two copy streams -- over groups of images for batches of small images,
+ * and INSIDE the image for images of 32 MiB and more (rows go up in chunks,
+ * each chunk's row pass runs as it lands, each block of whole column-pass
+ * segments runs as soon as the rows it reads are there and its output rows go
+ * down at once), so a single 16384^2 image moves at the PCIe full-duplex rate.
+ * Results are bitwise those of pl_snlm_2d_row_col.  Blocks until done. */
 int pl_snlm_2d_row_col_host(const float* host_src, float* host_dst, int32_t batch, int32_t rows,
                             int32_t cols, pl_params p, void* stream);
 

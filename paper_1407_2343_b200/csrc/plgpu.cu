@@ -13,6 +13,7 @@
 #include <limits>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "plgpu.h"
 #include "plgpu_aux.cuh"
@@ -1071,6 +1072,151 @@ int pl_snlm_2d(const float* src, float* dst, float* work, int32_t batch, int32_t
   return rc_passes(src, dst, mid, batch, rows, cols, p, as_stream(stream), cr_img);
 }
 
+namespace {
+
+// Host-buffer RC of LARGE images, streamed inside the image: rows go up in
+// chunks (H2D engine), each chunk's row pass runs as it lands, and as soon as
+// the rows a block of column-pass segments reads are present
+// (col_window: whole segments, so the result is bitwise the full pass's) that
+// block's column pass runs and its output rows go down (D2H engine).  Upload,
+// both passes and download of one image overlap; a 16384^2 image (1 GiB each
+// way) takes ~max(H2D, D2H) instead of H2D + passes + D2H.
+int host_rc_streamed(const float* host_src, float* host_dst, int32_t batch, int32_t rows,
+                     int32_t cols, const pl_params& p, cudaStream_t st) {
+  const size_t img = (size_t)rows * cols;
+  const int32_t S_col = std::min<int32_t>(p.search_radius, rows - 1);
+  const int32_t C = segment_length(rows, S_col);
+  const int32_t nseg = (rows + C - 1) / C;
+  const size_t row_bytes = (size_t)cols * sizeof(float);
+  // Chunk sizes by WARPS, not bytes: a pass launch takes at least one segment
+  // walk (c5: ~0.45 ms) however few lines it has, and the launches of one
+  // image run back to back on `st`, so each should fill the GPU (~148 x 8
+  // warps of 32 lines) -- capped at a quarter of the image so that uploads,
+  // passes and downloads still overlap (c3: 4 row chunks, 5 column blocks).
+  const int32_t S_row = std::min<int32_t>(p.search_radius, cols - 1);
+  const int32_t C_row = segment_length(cols, S_row);
+  const int32_t nseg_row = (cols + C_row - 1) / C_row;
+  constexpr int64_t kWave = 148 * 8;
+  auto up64 = [](int64_t v) { return (v + 63) / 64 * 64; };
+  const int32_t chunk_rows = (int32_t)std::min<int64_t>(
+      rows, std::max<int64_t>(64, std::min<int64_t>(up64((kWave + nseg_row - 1) / nseg_row * 32),
+                                                    up64((rows + 3) / 4))));
+  const int64_t warps_per_seg = std::max<int64_t>(1, cols / 32);
+  const int32_t segs_per_block = (int32_t)std::max<int64_t>(
+      1, std::min<int64_t>((kWave + warps_per_seg - 1) / warps_per_seg, nseg / 4));
+  // Copy streams and events are kept per host thread and device between calls
+  // (the call blocks until its pipeline has drained, so they are idle again).
+  struct Pipe {
+    int dev = -1;
+    cudaStream_t s_in = nullptr, s_out = nullptr;
+    std::vector<cudaEvent_t> ev;
+    size_t used = 0;
+    void reset() {
+      for (cudaEvent_t e : ev) cudaEventDestroy(e);
+      ev.clear();
+      if (s_in) cudaStreamDestroy(s_in);
+      if (s_out) cudaStreamDestroy(s_out);
+      s_in = s_out = nullptr;
+    }
+    ~Pipe() { reset(); }
+    int open() {
+      int d = 0;
+      PL_CUDA(cudaGetDevice(&d));
+      if (d != dev) {
+        reset();
+        dev = d;
+      }
+      if (!s_in) PL_CUDA(cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking));
+      if (!s_out) PL_CUDA(cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking));
+      used = 0;
+      return PL_OK;
+    }
+    int event(cudaEvent_t* out) {
+      if (used == ev.size()) {
+        cudaEvent_t e = nullptr;
+        PL_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        ev.push_back(e);
+      }
+      *out = ev[used++];
+      return PL_OK;
+    }
+  };
+  thread_local Pipe pipe;
+  if (int r = pipe.open()) return r;
+  Scratch scratch(st);
+  float* buf = nullptr;
+  int rc = scratch.alloc(3 * img * sizeof(float), &buf);
+  if (rc) return rc;
+  float* in = buf;
+  float* mid = buf + img;  // transposed intermediate [cols][rows] (rc_passes)
+  float* out = buf + 2 * img;
+  cudaEvent_t start = nullptr, drained = nullptr;
+  if ((rc = pipe.event(&start)) || (rc = pipe.event(&drained))) return rc;
+  PL_CUDA(cudaEventRecord(start, st));  // after the caller's prior work and the allocation
+  PL_CUDA(cudaStreamWaitEvent(pipe.s_in, start, 0));
+  auto image = [&](int b) -> int {
+    const float* hs = host_src + (size_t)b * img;
+    float* hd = host_dst + (size_t)b * img;
+    int32_t uploaded = 0;
+    for (int32_t a = 0; a < nseg; a += segs_per_block) {
+      const int32_t bb = std::min(nseg, a + segs_per_block);
+      int32_t in_lo, in_hi, out_lo, out_hi;
+      col_window(rows, S_col, p.patch_radius, a, bb, &in_lo, &in_hi, &out_lo, &out_hi);
+      const int32_t need = std::min<int64_t>(rows, ((int64_t)in_hi + 63) / 64 * 64);
+      while (uploaded < need) {
+        const int32_t r0 = uploaded, r1 = std::min(rows, r0 + chunk_rows);
+        cudaEvent_t up = nullptr;
+        if (int r = pipe.event(&up)) return r;
+        PL_CUDA(cudaMemcpyAsync(in + (size_t)r0 * cols, hs + (size_t)r0 * cols,
+                                (size_t)(r1 - r0) * row_bytes, cudaMemcpyHostToDevice, pipe.s_in));
+        PL_CUDA(cudaEventRecord(up, pipe.s_in));
+        PL_CUDA(cudaStreamWaitEvent(st, up, 0));
+        plgpu::PassDesc rp = row_desc(in + (size_t)r0 * cols, mid + r0, 1, r1 - r0, cols);
+        rp.dst_line_stride = 1;  // row r becomes column r of the transposed intermediate
+        rp.dst_pos_stride = rows;
+        if (int r = run_pass(rp, p, st)) return r;
+        uploaded = r1;
+      }
+      plgpu::PassDesc cp = col_desc(mid, out, 1, rows, cols);
+      cp.src_line_stride = rows;
+      cp.src_pos_stride = 1;
+      cp.seg_begin = a;
+      cp.nseg = bb - a;
+      if (int r = run_pass(cp, p, st)) return r;
+      cudaEvent_t done = nullptr;
+      if (int r = pipe.event(&done)) return r;
+      PL_CUDA(cudaEventRecord(done, st));
+      PL_CUDA(cudaStreamWaitEvent(pipe.s_out, done, 0));
+      PL_CUDA(cudaMemcpyAsync(hd + (size_t)out_lo * cols, out + (size_t)out_lo * cols,
+                              (size_t)(out_hi - out_lo) * row_bytes, cudaMemcpyDeviceToHost,
+                              pipe.s_out));
+    }
+    if (b + 1 < batch) {  // the next image reuses the three buffers
+      cudaEvent_t passes = nullptr, down = nullptr;
+      if (int r = pipe.event(&passes)) return r;
+      if (int r = pipe.event(&down)) return r;
+      PL_CUDA(cudaEventRecord(passes, st));
+      PL_CUDA(cudaStreamWaitEvent(pipe.s_in, passes, 0));  // `in` is free once its row passes ran
+      PL_CUDA(cudaEventRecord(down, pipe.s_out));
+      PL_CUDA(cudaStreamWaitEvent(st, down, 0));  // `out` is free once it is downloaded
+    }
+    return PL_OK;
+  };
+  for (int b = 0; b < batch && !rc; ++b) rc = image(b);
+  cudaError_t e0 = cudaEventRecord(drained, pipe.s_out);
+  if (e0 == cudaSuccess) e0 = cudaStreamWaitEvent(st, drained, 0);  // scratch freed after the last download
+  const cudaError_t e1 = cudaStreamSynchronize(pipe.s_out);
+  const cudaError_t e2 = cudaStreamSynchronize(pipe.s_in);
+  const cudaError_t e3 = cudaStreamSynchronize(st);
+  if (rc) return rc;
+  for (cudaError_t e : {e0, e1, e2, e3})
+    if (e != cudaSuccess)
+      return set_err(PL_ERR_CUDA, std::string("host pipeline: ") + cudaGetErrorString(e));
+  return check_launch();
+}
+
+}  // namespace
+
 int pl_snlm_2d_row_col_host(const float* host_src, float* host_dst, int32_t batch, int32_t rows,
                             int32_t cols, pl_params p, void* stream) {
   int rc = validate_image(batch, rows, cols);
@@ -1099,6 +1245,9 @@ int pl_snlm_2d_row_col_host(const float* host_src, float* host_dst, int32_t batc
     }
     precise = hi >= lo && p.h < kFastH * ((double)hi - (double)lo) / 255.0;
   }
+  // large images: stream rows / column-pass segments inside the image
+  if (!precise && img * sizeof(float) >= (32u << 20) && rows >= 1024)
+    return host_rc_streamed(host_src, host_dst, batch, rows, cols, p, st);
   const int per = (int)std::max<size_t>(1, std::min<size_t>(batch, (8u << 20) / (img * 4) + 1));
   const int ngroups = (batch + per - 1) / per;
   constexpr int NSLOT = 3;

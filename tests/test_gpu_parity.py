@@ -412,6 +412,23 @@ def test_host_e2e_matches_device():
     assert np.array_equal(dev_out, host_out)
 
 
+@pytest.mark.parametrize("shape,p", [
+    ((1, 1100, 8200), (10, 3, 74.8)),   # 3 column segments, 1 per block
+    ((2, 5000, 1800), (15, 5, 140.0)),  # 11 segments, two images through the same buffers
+    ((1, 9000, 1000), (25, 7, 136.9)),  # 8+ segments (multiple of 8), interior/edge bodies
+])
+def test_host_e2e_streamed_large_images(shape, p):
+    """Images of 32 MiB and more go through pl_snlm_2d_row_col_host's
+    intra-image pipeline (row chunks up, row pass per chunk, column pass per
+    block of whole segments as soon as its rows are there, output rows down):
+    bitwise the device result."""
+    rng = np.random.default_rng(shape[1])
+    imgs = rng.uniform(0, 255, shape).astype(np.float32)
+    dev_out = host(pl.snlm_2d_row_col(dev(imgs), p))
+    host_out = pl.snlm_2d_row_col_host(imgs, p)
+    assert np.array_equal(dev_out, np.asarray(host_out))
+
+
 def test_validation_errors_raise():
     x = dev(np.ones((5, 9), np.float32))
     with pytest.raises(pl.ValidationError, match="patch radius exceeds signal length"):
@@ -719,7 +736,8 @@ def test_guard_bands_no_stray_access():
     rng = np.random.default_rng(77)
     G = 4096
     for (b, r, c) in [(1, 1, 1), (1, 5, 7), (2, 33, 70), (1, 70, 300), (3, 130, 97),
-                      (1, 600, 520), (1, 64, 2048)]:
+                      (1, 600, 520), (1, 64, 2048),
+                      (1, 3, 40000), (2, 5, 9000)]:  # few long rows: the folded 1D pass
         for (S, K) in [(0, 0), (1, 0), (4, 2), (10, 3), (15, 5), (25, 7), (10, 9), (40, 1)]:
             if K > min(r, c):
                 continue
