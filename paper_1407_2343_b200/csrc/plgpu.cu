@@ -1074,6 +1074,48 @@ int pl_snlm_2d(const float* src, float* dst, float* work, int32_t batch, int32_t
 
 namespace {
 
+// Copy streams and events are kept per host thread and device between calls
+// (the call blocks until its pipeline has drained, so they are idle again).
+struct HostPipe {
+  int dev = -1;
+  cudaStream_t s_in = nullptr, s_out = nullptr;
+  std::vector<cudaEvent_t> ev;
+  size_t used = 0;
+  void reset() {
+    for (cudaEvent_t e : ev) cudaEventDestroy(e);
+    ev.clear();
+    if (s_in) cudaStreamDestroy(s_in);
+    if (s_out) cudaStreamDestroy(s_out);
+    s_in = s_out = nullptr;
+  }
+  ~HostPipe() { reset(); }
+  int open() {
+    int d = 0;
+    PL_CUDA(cudaGetDevice(&d));
+    if (d != dev) {
+      reset();
+      dev = d;
+    }
+    if (!s_in) PL_CUDA(cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking));
+    if (!s_out) PL_CUDA(cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking));
+    used = 0;
+    return PL_OK;
+  }
+  int event(cudaEvent_t* out) {
+    if (used == ev.size()) {
+      cudaEvent_t e = nullptr;
+      PL_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      ev.push_back(e);
+    }
+    *out = ev[used++];
+    return PL_OK;
+  }
+};
+HostPipe& host_pipe() {
+  thread_local HostPipe pipe;
+  return pipe;
+}
+
 // Host-buffer RC of LARGE images, streamed inside the image: rows go up in
 // chunks (H2D engine), each chunk's row pass runs as it lands, and as soon as
 // the rows a block of column-pass segments reads are present
@@ -1104,44 +1146,7 @@ int host_rc_streamed(const float* host_src, float* host_dst, int32_t batch, int3
   const int64_t warps_per_seg = std::max<int64_t>(1, cols / 32);
   const int32_t segs_per_block = (int32_t)std::max<int64_t>(
       1, std::min<int64_t>((kWave + warps_per_seg - 1) / warps_per_seg, nseg / 4));
-  // Copy streams and events are kept per host thread and device between calls
-  // (the call blocks until its pipeline has drained, so they are idle again).
-  struct Pipe {
-    int dev = -1;
-    cudaStream_t s_in = nullptr, s_out = nullptr;
-    std::vector<cudaEvent_t> ev;
-    size_t used = 0;
-    void reset() {
-      for (cudaEvent_t e : ev) cudaEventDestroy(e);
-      ev.clear();
-      if (s_in) cudaStreamDestroy(s_in);
-      if (s_out) cudaStreamDestroy(s_out);
-      s_in = s_out = nullptr;
-    }
-    ~Pipe() { reset(); }
-    int open() {
-      int d = 0;
-      PL_CUDA(cudaGetDevice(&d));
-      if (d != dev) {
-        reset();
-        dev = d;
-      }
-      if (!s_in) PL_CUDA(cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking));
-      if (!s_out) PL_CUDA(cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking));
-      used = 0;
-      return PL_OK;
-    }
-    int event(cudaEvent_t* out) {
-      if (used == ev.size()) {
-        cudaEvent_t e = nullptr;
-        PL_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-        ev.push_back(e);
-      }
-      *out = ev[used++];
-      return PL_OK;
-    }
-  };
-  thread_local Pipe pipe;
+  HostPipe& pipe = host_pipe();
   if (int r = pipe.open()) return r;
   Scratch scratch(st);
   float* buf = nullptr;
@@ -1252,23 +1257,15 @@ int pl_snlm_2d_row_col_host(const float* host_src, float* host_dst, int32_t batc
   const int ngroups = (batch + per - 1) / per;
   constexpr int NSLOT = 3;
   const size_t slot_elems = 3 * img * per;
-  struct Pipe {
-    cudaStream_t s_in = nullptr, s_out = nullptr;
-    cudaEvent_t ev[3 * NSLOT + 2] = {};
-    ~Pipe() {
-      for (cudaEvent_t e : ev)
-        if (e) cudaEventDestroy(e);
-      if (s_in) cudaStreamDestroy(s_in);
-      if (s_out) cudaStreamDestroy(s_out);
-    }
-  } pipe;
-  PL_CUDA(cudaStreamCreateWithFlags(&pipe.s_in, cudaStreamNonBlocking));
-  PL_CUDA(cudaStreamCreateWithFlags(&pipe.s_out, cudaStreamNonBlocking));
-  for (cudaEvent_t& e : pipe.ev) PL_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  cudaEvent_t* up = pipe.ev;
-  cudaEvent_t* done = pipe.ev + NSLOT;
-  cudaEvent_t* freed = pipe.ev + 2 * NSLOT;
-  cudaEvent_t start = pipe.ev[3 * NSLOT], drained = pipe.ev[3 * NSLOT + 1];
+  HostPipe& pipe = host_pipe();  // copy streams + events, kept per host thread
+  if ((rc = pipe.open())) return rc;
+  cudaEvent_t evs[3 * NSLOT + 2];
+  for (cudaEvent_t& e : evs)
+    if ((rc = pipe.event(&e))) return rc;
+  cudaEvent_t* up = evs;
+  cudaEvent_t* done = evs + NSLOT;
+  cudaEvent_t* freed = evs + 2 * NSLOT;
+  cudaEvent_t start = evs[3 * NSLOT], drained = evs[3 * NSLOT + 1];
   Scratch scratch(st);  // freed on st after `drained` (below)
   float* buf = nullptr;
   if ((rc = scratch.alloc(NSLOT * slot_elems * sizeof(float), &buf))) return rc;
