@@ -33,15 +33,17 @@
  *  - Boundary convention: half-sample mirror for patch content
  *    (core_types.cpp:71-88), search windows clipped to the line
  *    (nlm.cpp:71-73).  S larger than line-1 behaves as line-1.
- *  - Arithmetic: fp32.  Weights exp(-d/h^2) are ex2(-d') with d' the patch
- *    distance of samples prescaled by sqrt(log2 e)/h (computed in double on
- *    the host); quotients num/den by rcp, clamped into the range of the
- *    walked samples (constant inputs are exact fixpoints, outputs stay in
- *    the convex hull).  The distance-band exports are exact (bit-equal to
+ *  - Arithmetic: fp32 (double for calls the precision policy routes there).
+ *    Weights exp(-d/h^2) are ex2(-d') with d' the patch distance of samples
+ *    prescaled by sqrt(log2 e)/h (computed in double on the host); quotients
+ *    num/den by rcp, clamped into the range of the walked samples (constant
+ *    inputs are exact fixpoints, outputs stay in the convex hull).  The distance-band exports are exact (bit-equal to
  *    the reference) on integer-valued inputs.
  *  - Results are bitwise independent of batch size, line count, GPU count and
  *    of which axis a line lies on (row and column passes run identical per-
- *    line arithmetic), so transpose equivariance holds bit for bit.
+ *    line arithmetic), so transpose equivariance holds bit for bit -- within
+ *    one arithmetic route: under PL_PRECISION_AUTO a call with h < 40 picks
+ *    fp32 or double from its own data range (pl_set_precision_policy below).
  */
 #ifndef PLGPU_H_
 #define PLGPU_H_

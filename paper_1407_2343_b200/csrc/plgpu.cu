@@ -560,6 +560,7 @@ int choose_precise(const float* src, int64_t lines, int32_t n, int64_t ld, doubl
   const int64_t total = lines * n;
   const unsigned blocks = (unsigned)std::min<int64_t>((total + 255) / 256, 148 * 8);
   plgpu::range_kernel<<<blocks, 256, 0, st>>>(src, lines, n, ld, mm);
+  if ((rc = check_launch())) return rc;
   PL_CUDA(cudaMemcpyAsync(got, mm, sizeof got, cudaMemcpyDeviceToHost, st));
   PL_CUDA(cudaStreamSynchronize(st));
   if (got[0] > got[1]) return PL_OK;  // no finite sample
@@ -582,6 +583,7 @@ int run_precise(const float* src, float* dst, int64_t lines, int32_t n, int64_t 
   if (rc) return rc;
   const unsigned blocks = (unsigned)std::min<int64_t>((cnt + 255) / 256, 148 * 16);
   plgpu::widen_kernel<<<blocks, 256, 0, st>>>(src, buf, lines, n, ld);
+  if ((rc = check_launch())) return rc;
   if ((rc = call(buf, buf + cnt, buf + 2 * cnt))) return rc;
   plgpu::narrow_kernel<<<blocks, 256, 0, st>>>(buf + cnt, dst, lines, n, ld);
   return check_launch();
