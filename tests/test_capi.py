@@ -133,3 +133,19 @@ def test_bench_reference_arm_runs_on_cpu(tmp_path):
     assert line["unit"] == "Mpixel/s" and line["higher_is_better"] is True
     assert line["cpu_baseline"]["kind"] == "reference"
     assert line["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def test_precision_policy_api_host_only():
+    """pl_set_precision_policy / pl_precision_policy / pl_fast_h_threshold touch
+    no device: default AUTO, FAST round-trips, anything else is PL_ERR_ARG."""
+    L = pl.lib()
+    assert L.pl_precision_policy() == pl.PL_PRECISION_AUTO
+    assert L.pl_fast_h_threshold() == 40.0
+    with pl.precision_policy("fast"):
+        assert L.pl_precision_policy() == pl.PL_PRECISION_FAST
+    assert L.pl_precision_policy() == pl.PL_PRECISION_AUTO
+    assert L.pl_set_precision_policy(7) == pl.PL_ERR_ARG
+    assert b"precision policy" in L.pl_last_error()
+    assert L.pl_debug_set_route(3, 0, 0) == pl.PL_OK  # walker 3: 1D lines never folded
+    assert L.pl_debug_set_route(4, 0, 0) == pl.PL_ERR_ARG
+    assert L.pl_debug_set_route(0, 0, 0) == pl.PL_OK
