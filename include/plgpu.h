@@ -107,7 +107,8 @@ int pl_debug_set_route(int32_t walker, int32_t lines, int32_t wpc);
  * out: plgpu_walk64.cuh), slower but within the bound at any h.
  * PL_PRECISION_FAST: always the fp32 kernels.  Process-wide.  The partition-
  * level entry points (strided / blocked / window / fan-out passes, graphs)
- * are fp32 only. */
+ * are fp32 only: under PL_PRECISION_AUTO they return PL_ERR_UNSUPPORTED for
+ * h below the threshold instead of silently exceeding the bound. */
 enum pl_precision_policy { PL_PRECISION_AUTO = 0, PL_PRECISION_FAST = 1 };
 int pl_set_precision_policy(int32_t policy);
 int32_t pl_precision_policy(void);

@@ -569,6 +569,17 @@ int choose_precise(const float* src, int64_t lines, int32_t n, int64_t ld, doubl
   return PL_OK;
 }
 
+// The partition-level entry points (strided / blocked / window / fan-out
+// passes) run the fp32 kernels only: under PL_PRECISION_AUTO they refuse an h
+// the fp32 kernels are not bounded for instead of silently exceeding the
+// output tolerance (the caller confirms with PL_PRECISION_FAST).
+int require_fp32_bounded(double h) {
+  if (g_policy.load(std::memory_order_relaxed) == PL_PRECISION_FAST || h >= kFastH) return PL_OK;
+  return set_err(PL_ERR_UNSUPPORTED,
+                 "this entry point runs the fp32 kernels only and h is below their bounded range "
+                 "(pl_fast_h_threshold); use the whole-image entry points or PL_PRECISION_FAST");
+}
+
 // fp32 buffers through an fp64 entry point: widen into stream-ordered
 // scratch, `call(src64, dst64, work64)`, narrow.  `work_doubles` = the fp64
 // composite's own workspace.
@@ -838,6 +849,7 @@ int pl_nlm_col_pass_window(const float* src, int32_t in_lo, int32_t in_rows, flo
   if (!rc) rc = validate_params(p, rows_total);
   if (!rc) rc = check_ptrs(src, dst);
   if (rc) return rc;
+  if ((rc = require_fp32_bounded(p.h))) return rc;
   int32_t need_lo, need_hi, out_lo, out_hi;
   if ((rc = pl_col_window(rows_total, seg_begin, seg_end, p, &need_lo, &need_hi, &out_lo,
                           &out_hi)))
@@ -869,6 +881,7 @@ int pl_nlm_pass_strided(const float* src, float* dst, int32_t batch, int32_t lin
   if (!rc) rc = validate_params(p, n);
   if (!rc) rc = check_ptrs(src, dst);
   if (rc) return rc;
+  if ((rc = require_fp32_bounded(p.h))) return rc;
   if (src_line_stride < 0 || src_pos_stride < 1 || dst_line_stride < 0 || dst_pos_stride < 1 ||
       img_stride < 0)
     return set_err(PL_ERR_ARG, "strides must be nonnegative (position strides positive)");
@@ -894,6 +907,7 @@ int pl_nlm_row_pass_fanout(const float* src, float* dst, int32_t rows, int32_t c
   if (!rc) rc = validate_params(p, cols);
   if (!rc) rc = check_ptrs(src, dst);
   if (rc) return rc;
+  if ((rc = require_fp32_bounded(p.h))) return rc;
   if (n_extra < 0 || n_extra > PL_MAX_FANOUT || (n_extra > 0 && (!extra || !lo || !hi)))
     return set_err(PL_ERR_ARG, "n_extra must be 0..PL_MAX_FANOUT with extra/lo/hi arrays");
   for (int x = 0; x < n_extra; ++x)
@@ -925,6 +939,7 @@ int pl_nlm_row_pass_blocked(const float* src, float* dst, int32_t batch, int32_t
   if (!rc) rc = validate_params(p, cols);
   if (!rc) rc = check_ptrs(src, dst);
   if (rc) return rc;
+  if ((rc = require_fp32_bounded(p.h))) return rc;
   if (col_block < 1 || cols % col_block != 0)
     return set_err(PL_ERR_ARG, "cols must be a positive multiple of col_block");
   plgpu::PassDesc g = row_desc(src, dst, batch, rows, cols);

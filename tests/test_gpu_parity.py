@@ -229,7 +229,12 @@ def test_precision_policy_routes(orc):
     assert not pl.last_route().startswith("f64"), pl.last_route()
     want = orc.filter("rc", unit.astype(np.float64), 10, 3, 0.3, threads=4)
     assert np.abs(got.astype(np.float64) - want).max() <= T2 / 255.0
+    # the partition-level entry points are fp32 only: they refuse such an h
+    # unless the caller pins the fp32 kernels
+    with pytest.raises(RuntimeError, match="runs the fp32 kernels only"):
+        pl.nlm_row_pass_blocked(x, (10, 3, 12.0), 65)
     with pl.precision_policy("fast"):
+        pl.nlm_row_pass_blocked(x, (10, 3, 12.0), 65)
         fast = host(pl.snlm_2d_row_col(x, (10, 3, 12.0)))
         assert not pl.last_route().startswith("f64"), pl.last_route()
         g = pl.RCGraph(x, (10, 3, 12.0))  # allowed when pinned fast
