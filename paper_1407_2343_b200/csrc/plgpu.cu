@@ -76,11 +76,14 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 // walker.  Lines of 8192+ samples use a multiple of 8 segments, so that the
 // row-partitioned multi-GPU column pass (whole segments per rank) splits
 // evenly over 2, 4 or 8 GPUs.  Signal-length lines (32768+ samples: 1D
-// signals, processed one or a few at a time) use ~64-sample segments so a
-// single line still spreads over enough threads: c1 (one 65,536-sample
-// line) 195 -> ~1,000 Msample/s on the B200 for S/64 extra pre-walk.  Short
-// lines (<= 1024 samples: small images, a few hundred lines each) also use
+// signals, processed one or a few at a time) use ~32-sample segments so a
+// single line still spreads over enough lanes (the folded pass of
+// plgpu_walk3.cuh puts one segment on each lane): c1 (one 65,536-sample
+// line) 11.7 us per call vs 15.9 us at ~64, for S/32 extra pre-walk.  Short
+// lines (<= 1024 samples: small images, a few hundred lines each) use
 // ~64-sample segments, so a 512^2 image runs 64 warps instead of 16.
+// (build-variant knobs for the segment-length sweeps of profiles/README.md;
+// the shipped values are the defaults -- a different value changes result bits)
 #ifndef PLGPU_SEG_MID
 #define PLGPU_SEG_MID 480
 #endif

@@ -33,12 +33,15 @@
 #include "plgpu_walk2.cuh"
 
 
+// Build-variant knobs (tools/build_variant.py -D...): compile-time A/B switches
+// behind the measured tables of profiles/README.md.  The defaults are the
+// shipped kernels; none is read at run time and none changes a result bit.
 #ifndef PLGPU_PK1
 #define PLGPU_PK1 1  // 1-line kernels: {num, den} packed (FFMA2); 0 = scalar accumulators
 #endif
 
 #ifndef PLGPU_PK_REFILL_RING
-#define PLGPU_PK_REFILL_RING 1  // packed 1-line form: refill {x', s} from the nr ring (else LDS + scale)
+#define PLGPU_PK_REFILL_RING 1  // packed 1-line form with prescaled sums: refill {x', 1} from the nr ring (else LDS + scale)
 #endif
 #ifndef PLGPU_LOCK_WPC
 #define PLGPU_LOCK_WPC 8   // warps per lockstep CTA
