@@ -43,6 +43,9 @@
 #ifndef PLGPU_PK_REFILL_RING
 #define PLGPU_PK_REFILL_RING 1  // packed 1-line form with prescaled sums: refill {x', 1} from the nr ring (else LDS + scale)
 #endif
+#ifndef PLGPU_EARLY_REFILL
+#define PLGPU_EARLY_REFILL 1  // 1-line kernels, S <= 16: the step's refill loads are issued ahead of its pair loop
+#endif
 #ifndef PLGPU_LOCK_WPC
 #define PLGPU_LOCK_WPC 8   // warps per lockstep CTA
 #endif
@@ -394,6 +397,15 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
         if (MASK && s >= T) break;
         const int i = i0 + s;
         const V an_ = nr[r], ao = orr[r];
+        // 1-line S = 15: the three refill loads of the step go out before its pair
+        // loop instead of after it (c3 +0.9 %; S = 25, at 255 registers, -0.5 %)
+        constexpr bool EARLY = PLGPU_EARLY_REFILL && LINES == 1 && !AP && ST <= 16;
+        V e_fnew = zero, e_orr = zero, e_xr = zero;
+        if constexpr (EARLY) {
+          e_fnew = at(r, 2 + KT + ST);
+          e_orr = at(r, 1 + ST);
+          e_xr = at(r, BASE);
+        }
         const int kmax = MASK ? min(S, n - 1 - i) : ST;
         V qv;
         if constexpr (PK) {
@@ -474,7 +486,7 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
             frp[r] = f2_set_lo(frp[r], fs1);
           }
         } else {
-          const V fnew = at(r, 2 + KT + ST);
+          const V fnew = EARLY ? e_fnew : at(r, 2 + KT + ST);
           if constexpr (!PAIR) track(fnew);
           // {f, 1}: keeping the 1.0 half in place measured c3 +1.4 %, c5 -22 % (register
           // allocation at 255 registers), so only for S <= 16
@@ -488,12 +500,12 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
         // kernel) or re-read from the staged chunk and scaled (1-line kernels:
         // the copy's register shuffles cost c3 2.5 %; S = 25 spills with it).
         if constexpr (2 * KT < ST && ST <= 16 && LINES == 2) orr[r] = nr[(r + R - 2 * KT - 1) % R];
-        else orr[r] = sc(at(r, 1 + ST));
+        else orr[r] = sc(EARLY ? e_orr : at(r, 1 + ST));
         // Packed prescale (one FMUL2 instead of two FMULs: c4 +2.3 %) where
         // the scaled sample feeds many subtractions (the nr ring doubles as
         // the orr ring), so ptxas has no single-use product it could contract
         // into a following subtraction; bitwise equal to the scalar form.
-        const V xr = at(r, BASE);  // raw x_s: distance ring and clamp range
+        const V xr = EARLY ? e_xr : at(r, BASE);  // raw x_s: distance ring and clamp range
         if constexpr (LINES == 2 && 2 * KT < ST && ST <= 16) nr[r] = Ops::mul(xr, svv);
         else nr[r] = sc(xr);
         if constexpr (PAIR) {
