@@ -43,8 +43,16 @@
 #ifndef PLGPU_PK_REFILL_RING
 #define PLGPU_PK_REFILL_RING 1  // packed 1-line form with prescaled sums: refill {x', 1} from the nr ring (else LDS + scale)
 #endif
-#ifndef PLGPU_EARLY_REFILL
-#define PLGPU_EARLY_REFILL 1  // 1-line kernels, S <= 16: the step's refill loads are issued ahead of its pair loop
+// refill loads issued ahead of the step's pair loop, per template radius:
+// bit 0 = entering f, bit 1 = leaving partner, bit 2 = entering x
+#ifndef PLGPU_EARLY_S10
+#define PLGPU_EARLY_S10 0
+#endif
+#ifndef PLGPU_EARLY_S15
+#define PLGPU_EARLY_S15 7
+#endif
+#ifndef PLGPU_EARLY_S25
+#define PLGPU_EARLY_S25 0
 #endif
 #ifndef PLGPU_LOCK_WPC
 #define PLGPU_LOCK_WPC 8   // warps per lockstep CTA
@@ -397,15 +405,16 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
         if (MASK && s >= T) break;
         const int i = i0 + s;
         const V an_ = nr[r], ao = orr[r];
-        // 1-line S = 15: the three refill loads of the step go out before its pair
-        // loop instead of after it (c3 +0.9 %; S = 25, at 255 registers, -0.5 %)
-        constexpr bool EARLY = PLGPU_EARLY_REFILL && LINES == 1 && !AP && ST <= 16;
+        // Source order of the step's refill loads (positions fixed by the
+        // step, not by the rings): ahead of the pair loop for the 1-line S = 15
+        // kernel (c3 +0.9 %; S = 25, at 255 registers, -0.5 %).
+        constexpr int EARLY = ST <= 10 ? PLGPU_EARLY_S10 : ST <= 16 ? (LINES == 1 ? PLGPU_EARLY_S15 : 0)
+                                                                    : PLGPU_EARLY_S25;
+        constexpr bool E_F = (EARLY & 1) && !AP, E_O = (EARLY & 2) != 0, E_X = (EARLY & 4) != 0;
         V e_fnew = zero, e_orr = zero, e_xr = zero;
-        if constexpr (EARLY) {
-          e_fnew = at(r, 2 + KT + ST);
-          e_orr = at(r, 1 + ST);
-          e_xr = at(r, BASE);
-        }
+        if constexpr (E_F) e_fnew = at(r, 2 + KT + ST);
+        if constexpr (E_O && !(2 * KT < ST && ST <= 16 && LINES == 2)) e_orr = at(r, 1 + ST);
+        if constexpr (E_X) e_xr = at(r, BASE);
         const int kmax = MASK ? min(S, n - 1 - i) : ST;
         V qv;
         if constexpr (PK) {
@@ -486,7 +495,7 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
             frp[r] = f2_set_lo(frp[r], fs1);
           }
         } else {
-          const V fnew = EARLY ? e_fnew : at(r, 2 + KT + ST);
+          const V fnew = E_F ? e_fnew : at(r, 2 + KT + ST);
           if constexpr (!PAIR) track(fnew);
           // {f, 1}: keeping the 1.0 half in place measured c3 +1.4 %, c5 -22 % (register
           // allocation at 255 registers), so only for S <= 16
@@ -500,12 +509,12 @@ __device__ __forceinline__ void walk3(const Pass2Desc& g, float* ring, const int
         // kernel) or re-read from the staged chunk and scaled (1-line kernels:
         // the copy's register shuffles cost c3 2.5 %; S = 25 spills with it).
         if constexpr (2 * KT < ST && ST <= 16 && LINES == 2) orr[r] = nr[(r + R - 2 * KT - 1) % R];
-        else orr[r] = sc(EARLY ? e_orr : at(r, 1 + ST));
+        else orr[r] = sc(E_O ? e_orr : at(r, 1 + ST));
         // Packed prescale (one FMUL2 instead of two FMULs: c4 +2.3 %) where
         // the scaled sample feeds many subtractions (the nr ring doubles as
         // the orr ring), so ptxas has no single-use product it could contract
         // into a following subtraction; bitwise equal to the scalar form.
-        const V xr = EARLY ? e_xr : at(r, BASE);  // raw x_s: distance ring and clamp range
+        const V xr = E_X ? e_xr : at(r, BASE);  // raw x_s: distance ring and clamp range
         if constexpr (LINES == 2 && 2 * KT < ST && ST <= 16) nr[r] = Ops::mul(xr, svv);
         else nr[r] = sc(xr);
         if constexpr (PAIR) {
