@@ -42,7 +42,7 @@
  *  - Results are bitwise independent of batch size, line count, GPU count and
  *    of which axis a line lies on (row and column passes run identical per-
  *    line arithmetic), so transpose equivariance holds bit for bit -- within
- *    one arithmetic route: under PL_PRECISION_AUTO a call with h < 40 picks
+ *    one arithmetic route: under PL_PRECISION_AUTO a call with h < 48 picks
  *    fp32 or double from its own data range (pl_set_precision_policy below).
  */
 #ifndef PLGPU_H_
@@ -99,7 +99,7 @@ int pl_debug_set_route(int32_t walker, int32_t lines, int32_t wpc);
  * pl_snlm_2d, pl_snlm_2d_row_col_host).  The fp32 kernels hold the output
  * bound (max abs error 1e-3 on a [0, 255] scale against the reference's
  * double arithmetic) while h >= pl_fast_h_threshold() / 255 of the data range
- * (40: every setting of the configs).  PL_PRECISION_AUTO
+ * (48: every setting of the configs).  PL_PRECISION_AUTO
  * (default): calls with h >= the threshold run the fp32 kernels directly;
  * below it the input's range is measured (one reduction, the call then
  * synchronises `stream`) and, if h is under threshold/255 of it, the call runs

@@ -535,12 +535,13 @@ int check_ptrs(const void* a, const void* b) {
 // fp32 intermediate's quantisation by ~ 2 |df| |f - out| / h^2).  Under
 // PL_PRECISION_AUTO (default) the reference-API entry points therefore run
 // such calls in double on the device (plgpu_walk64.cuh: fp32 in, fp64
-// arithmetic and intermediates, fp32 out).  h >= 40 -- every 8-bit-scale
+// arithmetic and intermediates, fp32 out).  h >= 48 -- every 8-bit-scale
 // setting the fp32 kernels are bounded for -- goes straight to the fp32
 // kernels; below that the input's range is measured first (one reduction and a
-// stream synchronisation) and h is compared with 40/255 of it.
+// stream synchronisation) and h is compared with 48/255 of it.  (The fp32 composites reach 1.03e-3 at
+// h = 33 on 12,875-sample lines, K = 1, and scale like 1 / h^2: 0.5e-3 at 48.)
 std::atomic<int> g_policy{PL_PRECISION_AUTO};
-constexpr double kFastH = 40.0;  // per 255 of data range
+constexpr double kFastH = 48.0;  // per 255 of data range
 
 int choose_precise(const float* src, int64_t lines, int32_t n, int64_t ld, double h,
                    cudaStream_t st, bool* precise) {

@@ -140,7 +140,7 @@ def test_precision_policy_api_host_only():
     no device: default AUTO, FAST round-trips, anything else is PL_ERR_ARG."""
     L = pl.lib()
     assert L.pl_precision_policy() == pl.PL_PRECISION_AUTO
-    assert L.pl_fast_h_threshold() == 40.0
+    assert L.pl_fast_h_threshold() == 48.0
     with pl.precision_policy("fast"):
         assert L.pl_precision_policy() == pl.PL_PRECISION_FAST
     assert L.pl_precision_policy() == pl.PL_PRECISION_AUTO
